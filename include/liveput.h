@@ -1,0 +1,212 @@
+/*
+ * liveput.h — C ABI of the B200-native liveput planner (Parcae, arxiv 2403.14097).
+ *
+ * Drop-in boundary for the reference's planning hot path, `spotsim::Planner`
+ * (/root/reference/proj/core/include/spotsim/optimizer.hpp:41-92) and the free
+ * functions it sits on.  Every entry point below names the reference symbol it
+ * replaces.  Plain C types only: no torch, no C++ in the signatures.
+ *
+ * Conventions
+ *   - Every call returns an lp_status; LP_OK == 0.  Failures store a message
+ *     retrievable with lp_last_error(handle) (or lp_last_global_error() for
+ *     calls that have no handle).  The C++/Python facades map LP_EINVAL to
+ *     std::invalid_argument / ValueError, matching the reference's exceptions.
+ *   - A config with pipelines == 0 is the suspended state (the reference's
+ *     std::nullopt, optimizer.hpp:25).
+ *   - All buffers are caller-owned host memory unless the name says "_dev".
+ *   - One handle = one CUDA device, one stream, one host thread at a time
+ *     (the reference Planner is not thread-safe either, optimizer.hpp:38-40).
+ */
+#ifndef LIVEPUT_H_
+#define LIVEPUT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LP_OK = 0,
+  LP_EINVAL = 1,       /* bad argument; reference throws std::invalid_argument */
+  LP_ECUDA = 2,        /* CUDA runtime failure */
+  LP_ENOMEM = 3,       /* device or host allocation failed */
+  LP_EUNSUPPORTED = 4, /* outside the sizes this build supports */
+  LP_ENCCL = 5         /* NCCL failure */
+} lp_status;
+
+/* ParallelConfig (perf_model.hpp:10-16). pipelines == 0 -> suspended. */
+typedef struct {
+  int32_t pipelines; /* D */
+  int32_t stages;    /* P */
+} lp_config;
+
+/* WorkloadProfile (perf_model.hpp:26-49).  pipeline_rates is passed as two
+ * parallel arrays (depth, samples/s); n_rates may be 0. */
+typedef struct {
+  double compute_per_microbatch_s;
+  double param_bytes;
+  double activation_bytes;
+  int32_t minibatch_size;
+  int32_t microbatch_size;
+  double device_memory_bytes;
+  double memory_fixed_bytes;     /* MemoryModel::fixed_bytes */
+  double memory_per_stage_bytes; /* MemoryModel::per_stage_bytes */
+  double alpha_s;
+  double beta_s_per_byte;
+  int32_t n_rates;
+  const int32_t* rate_depths;
+  const double* rate_values;
+} lp_profile;
+
+/* CostTable (migration.hpp:16-27). */
+typedef struct {
+  double start_process_s;
+  double rendezvous_s;
+  double cuda_context_s;
+  double load_data_s;
+  double build_model_s;
+  double update_comm_groups_s;
+} lp_costs;
+
+/* PlannerOptions (optimizer.hpp:13-23). */
+typedef struct {
+  double interval_s;
+  int32_t lookahead;
+  int32_t mc_trials;
+  uint64_t exact_cap;
+  uint64_t mc_seed;
+  double rollback_penalty_s;
+  int32_t strict_conditional;
+} lp_options;
+
+/* PlanStep (optimizer.hpp:26-31). */
+typedef struct {
+  int32_t interval_index;
+  lp_config config;
+  double expected_committed;
+  double expected_mig_cost_s;
+} lp_plan_step;
+
+/* One row of the liveput table produced by a re-plan: the expected surviving
+ * throughput of `config` over interval `interval` (n_now -> n_next), i.e. the
+ * reference's expected_liveput (preemption.cpp:94-112) evaluated on the
+ * planner's scenario ensemble. */
+typedef struct {
+  int32_t interval; /* j: the transition n_seq[j] -> n_seq[j+1] */
+  lp_config config;
+  double liveput;
+} lp_liveput_row;
+
+/* Counters of the last lp_replan / lp_execute on this handle. */
+typedef struct {
+  uint64_t resolutions;      /* (scenario, prev-config) resolutions = reference tally() calls */
+  uint64_t scenarios;        /* distinct sampled/enumerated scenarios (all ranks) */
+  uint64_t local_scenarios;  /* scenarios this rank generated */
+  int32_t mc_pairs;          /* distinct (n, k) Monte-Carlo pairs */
+  int32_t exact_pairs;       /* distinct (n, k) exactly-enumerated pairs */
+  int32_t kernel_launches;   /* kernels launched by the last execute */
+  int32_t horizon;
+  double hist_ms;            /* device time of histogram kernels (CUDA events) */
+  double reduce_ms;          /* device time of the cross-rank histogram reduce */
+  double dp_ms;              /* device time of the DP kernels */
+  double total_ms;           /* device time of the whole execute */
+  uint64_t hist_alg_ops;     /* algorithmic int32-equivalent ops of the histogram kernel */
+  uint64_t h2d_bytes;        /* bytes copied host->device by the last prepare */
+  uint64_t d2h_bytes;        /* bytes copied device->host by the last fetch */
+} lp_stats;
+
+typedef struct lp_handle lp_handle;
+
+/* ---- handle lifecycle: Planner(WorkloadProfile, CostTable, PlannerOptions)
+ *      optimizer.hpp:43 / optimizer.cpp:27-28 ---------------------------- */
+lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_options* options,
+                    int32_t device, lp_handle** out);
+void lp_destroy(lp_handle* h);
+const char* lp_last_error(const lp_handle* h);
+const char* lp_last_global_error(void);
+lp_status lp_get_options(const lp_handle* h, lp_options* out);
+
+/* ---- the hot path: Planner::dp_optimize (optimizer.hpp:64-65,
+ *      optimizer.cpp:140-205).  n_seq has len >= 2 entries; out has len-1
+ *      steps.  liveput_out (nullable) receives up to liveput_cap rows; the row
+ *      count is written to *liveput_rows (nullable). ----------------------- */
+lp_status lp_replan(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len,
+                    lp_plan_step* out, lp_liveput_row* liveput_out, int32_t liveput_cap,
+                    int32_t* liveput_rows);
+
+/* lp_replan split in three so that device-resident throughput can be timed:
+ * prepare = host tables + one H2D upload, execute = kernels only (cold:
+ * recomputes every histogram), fetch = one D2H of the plan. */
+lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len);
+lp_status lp_execute(lp_handle* h);
+lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* liveput_out,
+                   int32_t liveput_cap, int32_t* liveput_rows);
+lp_status lp_get_stats(const lp_handle* h, lp_stats* out);
+/* The CUDA stream every kernel of this handle runs on (cudaStream_t as void*). */
+void* lp_stream(lp_handle* h);
+
+/* ---- Planner::phi (optimizer.hpp:57-58, optimizer.cpp:52-62, 96-138) ---- */
+lp_status lp_phi(lp_handle* h, lp_config prev, lp_config next, int32_t n_now, int32_t n_next,
+                 double* committed, double* mig_cost_s);
+
+/* ---- Planner::sequence_value (optimizer.hpp:69-71, optimizer.cpp:207-219) */
+lp_status lp_sequence_value(lp_handle* h, lp_config current, const lp_config* sequence,
+                            const int32_t* n_seq, int32_t len, double* out);
+
+/* ---- Planner::survivor_histogram (optimizer.cpp:64-94), un-normalised:
+ *      counts[m] for m = 0..D (D+1 entries), *total = scenario count.  ---- */
+lp_status lp_survivor_hist(lp_handle* h, lp_config prev, int32_t n_now, int32_t n_minus,
+                           uint64_t* counts, uint64_t* total);
+
+/* ---- expected_liveput with EvalMode (preemption.hpp:53-65,
+ *      preemption.cpp:94-112).  exact != 0 -> enumerate_vectors, else
+ *      sample_vectors(n, n_minus, trials, seed).  FP64; agrees with the
+ *      reference to ~1e-15 relative (summation order differs). ---------- */
+lp_status lp_expected_liveput(lp_handle* h, lp_config cfg, int32_t n, int32_t n_minus,
+                              int32_t exact, int32_t trials, uint64_t seed, double* out);
+
+/* ---- parity mode: per-(trial, config) survivor minimum m of
+ *      sample_vectors/enumerate_vectors + stage_survivors
+ *      (preemption.cpp:23-66).  out is trials x n_cfg, row-major (trial-major),
+ *      uint16 m.  exact != 0 -> trials must equal C(n, n_minus) and trial t is
+ *      the t-th vector of enumerate_vectors (lexicographic).  ------------- */
+lp_status lp_dump_survivors(lp_handle* h, int32_t n, int32_t n_minus, int32_t exact,
+                            int32_t trials, uint64_t seed, const lp_config* cfgs, int32_t n_cfg,
+                            uint16_t* out);
+
+/* ---- parity mode: the sampled preemption sets themselves, sorted ascending,
+ *      trials x n_minus uint16 (sample_vectors, preemption.cpp:47-59). ---- */
+lp_status lp_dump_scenarios(lp_handle* h, int32_t n, int32_t n_minus, int32_t trials,
+                            uint64_t seed, uint16_t* out);
+
+/* ---- multi-GPU: trials of every (n, k) pair are split across ranks and the
+ *      integer histograms are summed with one ncclAllReduce over NVLink. ---- */
+#define LP_NCCL_ID_BYTES 128
+lp_status lp_nccl_unique_id(uint8_t out[LP_NCCL_ID_BYTES]);
+lp_status lp_comm_init(lp_handle* h, const uint8_t id[LP_NCCL_ID_BYTES], int32_t nranks,
+                       int32_t rank);
+
+/* ---- host table producers (perf_model stays on the host):
+ *      throughput perf_model.cpp:14-42, enumerate_configs :44-52,
+ *      depth_feasible :5-8, reactive_plan optimizer.cpp:11-25,
+ *      scenario_count preemption.cpp:10-21, mix_seed rng.hpp:46-55. ------- */
+double lp_throughput(const lp_profile* profile, lp_config cfg);
+int32_t lp_depth_feasible(const lp_profile* profile, int32_t stages);
+/* Writes min(count, cap) configs in reference order; returns the full count. */
+int32_t lp_enumerate_configs(const lp_profile* profile, int32_t n, lp_config* out, int32_t cap);
+/* Writes the reactive choice; returns 1 if one exists, 0 if suspended. */
+int32_t lp_reactive_plan(const lp_profile* profile, int32_t n_now, lp_config* out);
+uint64_t lp_scenario_count(int32_t n, int32_t k);
+uint64_t lp_mix_seed(uint64_t a, uint64_t b);
+
+/* Build information (sm arch, sizes supported). */
+int32_t lp_max_instances(void);
+const char* lp_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIVEPUT_H_ */

@@ -1,0 +1,1235 @@
+// lp_api.cpp — the C ABI of include/liveput.h: host planner over the sm_100a
+// kernels.  The host side only builds tables (configs, throughput, costs,
+// ensemble descriptors) and launches; every histogram, phi, DP step and the
+// traceback run on the device.  There is no CPU fallback.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "liveput.h"
+#include "lp_launch.h"
+#include "lp_layout.h"
+#include "lp_model.hpp"
+
+namespace lp {
+namespace {
+
+thread_local std::string g_global_err;
+
+constexpr uint64_t kEnumerationCap = 1000000ULL;  // preemption.hpp:26
+constexpr size_t kSmemBudgetR = 72 * 1024;
+constexpr size_t kSmemBudgetC = 110 * 1024;
+constexpr uint64_t kChunkR = 256 * 8;
+
+size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// ---------------------------------------------------------------------------
+// growable device / pinned host buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 16);
+    want = want + want / 4;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 1 << 16);
+    want = want + want / 4;
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Sections appended to one host image and uploaded with a single copy.
+struct Packer {
+  std::vector<unsigned char> bytes;
+  size_t add(const void* src, size_t n) {
+    size_t off = (bytes.size() + 255) & ~size_t(255);
+    bytes.resize(off + std::max<size_t>(n, 1));
+    if (n && src) std::memcpy(bytes.data() + off, src, n);
+    else if (n) std::memset(bytes.data() + off, 0, n);
+    return off;
+  }
+  template <typename T>
+  size_t add(const std::vector<T>& v) {
+    return add(v.data(), v.size() * sizeof(T));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// histogram plan: ensembles -> pairs / entries / work items / launch groups
+struct EnsembleSpec {
+  int n = 0, k = 0;
+  bool exact = false;
+  uint64_t count = 0;  // ensemble size (all ranks)
+  uint64_t seed = 0;
+  std::map<int, int> dmax_by_p;  // depth -> largest D needed
+  uint64_t ref_keys = 0;         // distinct (D,P) keys the reference would tally
+};
+
+struct Group {
+  int kind = 0;  // 0: register variant, 1: counter variant
+  int kmax = 0;
+  int threads = 256;
+  bool smem_evt = true;
+  size_t smem = 0;
+  int pmax_cap = 0;
+  int first = 0, count = 0;
+};
+
+struct HistPlan {
+  std::vector<PairDesc> pairs;
+  std::vector<EntryDesc> entries;
+  std::vector<DrawConst> draws;
+  std::vector<uint64_t> binom;
+  std::vector<WorkItem> work;
+  std::vector<Group> groups;
+  int64_t evt_len = 0, h0_len = 0, hist_len = 0;
+  uint64_t scenarios = 0, local_scenarios = 0, resolutions = 0, alg_ops = 0;
+  int mc_pairs = 0, exact_pairs = 0;
+};
+
+int kmax_for(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : 16); }
+
+size_t smem_regs(int ne, int kmax, int n, int64_t evt_len, bool smem_evt) {
+  return a16(sizeof(EntryDesc) * ne) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
+         (smem_evt ? a16(4 * (size_t)evt_len) : 0);
+}
+
+size_t smem_ctr(int ne, int k, int n, int64_t evt_len, bool smem_evt, int T, int pmax) {
+  const size_t nw = (n + 31) / 32;
+  const size_t gen = 4 * (size_t)(k + nw) * T;
+  const size_t ctr = 4 * (size_t)((pmax + 3) / 4) * T;
+  return a16(sizeof(EntryDesc) * ne) + a16(sizeof(DrawConst) * k) + a16(4 * (size_t)n) +
+         (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(2 * (size_t)k * T) + a16(std::max(gen, ctr));
+}
+
+// Algorithmic int32-equivalent ops (restated for the
+// threshold-event resolution): S(k) = 20 + 35k per scenario,
+// R(k) = 6k per (scenario, depth); no per-(scenario, config) term.
+uint64_t alg_ops(uint64_t scen, int k, int depths) {
+  return scen * (20ull + 35ull * k + 6ull * k * (uint64_t)depths);
+}
+
+lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int nranks,
+                          HistPlan& hp, std::string& err) {
+  hp = HistPlan();
+  for (const EnsembleSpec& sp : specs) {
+    const int n = sp.n, k = sp.k;
+    if (n > kMaxN) {
+      err = "liveput: n exceeds the supported maximum of " + std::to_string(kMaxN);
+      return LP_EUNSUPPORTED;
+    }
+    PairDesc pd{};
+    pd.n = n;
+    pd.k = k;
+    pd.exact = sp.exact ? 1 : 0;
+    pd.entry_base = (int)hp.entries.size();
+    pd.n_entries = (int)sp.dmax_by_p.size();
+    pd.h0_off = (int)hp.h0_len;
+    hp.h0_len += std::max(n, 1);
+    pd.seed = sp.seed;
+    pd.count = sp.count;
+    pd.t_lo = sp.count * (uint64_t)rank / (uint64_t)nranks;
+    pd.t_hi = sp.count * (uint64_t)(rank + 1) / (uint64_t)nranks;
+    pd.variant = k <= kMaxKReg ? 0 : 1;
+    const int pair_idx = (int)hp.pairs.size();
+    int max_dm = 0;
+    for (const auto& [P, Dm] : sp.dmax_by_p) {
+      EntryDesc e{};
+      e.P = P;
+      e.Dmax = Dm;
+      e.lim = P * Dm;
+      e.magic = P >= 2 ? (uint32_t)((1ull << 32) / (uint64_t)P + 1ull) : 0u;
+      e.tmax = std::min(k, Dm);
+      e.evt_off = (int)hp.evt_len;
+      hp.evt_len += (int64_t)std::max(0, e.tmax - 1) * Dm;
+      e.hist_off = (int)hp.hist_len;
+      hp.hist_len += hist_row(Dm + 1, k);
+      e.pair = pair_idx;
+      max_dm = std::max(max_dm, Dm);
+      hp.entries.push_back(e);
+    }
+    if (pd.variant == 1 && k > kMaxK && max_dm > kMaxK) {
+      err = "liveput: n_minus > 255 with more than 255 pipelines per depth is not supported";
+      return LP_EUNSUPPORTED;
+    }
+    if (sp.exact) {
+      const int stride = std::min(k, n - k) + 1;
+      pd.binom_off = (int)hp.binom.size();
+      pd.binom_stride = stride;
+      const uint64_t sat = 1ull << 62;
+      std::vector<uint64_t> tab((size_t)(n + 1) * stride, 0);
+      for (int a = 0; a <= n; ++a)
+        for (int s = 0; s < stride && s <= a; ++s) {
+          uint64_t v;
+          if (s == 0 || s == a) v = 1;
+          else {
+            // C(a, s) = C(a-1, s-1) + C(a-1, s); indices stay within the
+            // small side since s <= stride - 1
+            const uint64_t x = tab[(size_t)(a - 1) * stride + (s - 1)];
+            const uint64_t y = (s <= a - 1) ? tab[(size_t)(a - 1) * stride + s] : 0;
+            v = std::min(sat, x + y);
+          }
+          tab[(size_t)a * stride + s] = v;
+        }
+      hp.binom.insert(hp.binom.end(), tab.begin(), tab.end());
+      hp.exact_pairs++;
+    } else {
+      pd.draw_off = (int)hp.draws.size();
+      for (int i = 0; i < k; ++i) {
+        DrawConst d{};
+        d.b = (uint32_t)(n - i);
+        d.lim = UINT64_MAX - UINT64_MAX % d.b;
+        d.fm = UINT64_MAX / d.b + 1;
+        d.c32 = (uint32_t)((1ull << 32) % d.b);
+        hp.draws.push_back(d);
+      }
+      hp.mc_pairs++;
+    }
+    hp.pairs.push_back(pd);
+    const uint64_t local = pd.t_hi - pd.t_lo;
+    hp.scenarios += sp.count;
+    hp.local_scenarios += local;
+    hp.resolutions += sp.count * sp.ref_keys;
+    hp.alg_ops += alg_ops(local, k, pd.n_entries);
+  }
+
+  // work items, grouped by launch configuration
+  std::map<std::tuple<int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
+  for (int pi = 0; pi < (int)hp.pairs.size(); ++pi) {
+    const PairDesc& pd = hp.pairs[pi];
+    const uint64_t local = pd.t_hi - pd.t_lo;
+    if (local == 0 || pd.n_entries == 0) continue;
+    const int e_end = pd.entry_base + pd.n_entries;
+    if (pd.variant == 0) {
+      const int km = kmax_for(pd.k);
+      int e = pd.entry_base;
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        // grow the range while it fits the shared-memory budget
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && smem_regs(e2 - e + 1, km, pd.n, ev2, true) > kSmemBudgetR) break;
+          ev = ev2;
+          ++e2;
+        }
+        const bool sm = smem_regs(e2 - e, km, pd.n, ev, true) <= kSmemBudgetR;
+        const size_t smem = smem_regs(e2 - e, km, pd.n, ev, sm);
+        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += kChunkR) {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.t0 = t0;
+          w.t1 = std::min(pd.t_hi, t0 + kChunkR);
+          groups[{0, km, 256, sm ? 1 : 0}].push_back({w, {smem, 0}});
+        }
+        e = e2;
+      }
+    } else {
+      // counter variant: pick the widest block whose single-depth range fits
+      int pmax_all = 0;
+      for (int e = pd.entry_base; e < e_end; ++e) pmax_all = std::max(pmax_all, hp.entries[e].P);
+      int T = 128;
+      while (T > 32 && smem_ctr(1, pd.k, pd.n, 0, false, T, pmax_all) > kSmemBudgetC) T >>= 1;
+      int e = pd.entry_base;
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && smem_ctr(e2 - e + 1, pd.k, pd.n, ev2, true, T, x.P) > kSmemBudgetC) break;
+          ev = ev2;
+          ++e2;
+        }
+        const int pmax = hp.entries[e2 - 1].P;  // entries ascend in P
+        const bool sm = smem_ctr(e2 - e, pd.k, pd.n, ev, true, T, pmax) <= kSmemBudgetC;
+        const size_t smem = smem_ctr(e2 - e, pd.k, pd.n, ev, sm, T, pmax);
+        const uint64_t chunk = (uint64_t)T * 8;
+        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.t0 = t0;
+          w.t1 = std::min(pd.t_hi, t0 + chunk);
+          groups[{1, 0, T, sm ? 1 : 0}].push_back({w, {smem, pmax}});
+        }
+        e = e2;
+      }
+    }
+  }
+  for (auto& [key, items] : groups) {
+    Group g;
+    g.kind = std::get<0>(key);
+    g.kmax = std::get<1>(key);
+    g.threads = std::get<2>(key);
+    g.smem_evt = std::get<3>(key) != 0;
+    g.first = (int)hp.work.size();
+    g.count = (int)items.size();
+    for (auto& it : items) {
+      g.pmax_cap = std::max(g.pmax_cap, it.second.second);
+    }
+    for (auto& it : items) {
+      hp.work.push_back(it.first);
+      size_t s = it.second.first;
+      if (g.kind == 1) {
+        const PairDesc& pd = hp.pairs[it.first.pair];
+        s = smem_ctr(it.first.e_hi - it.first.e_lo, pd.k, pd.n, it.first.evt_len, g.smem_evt,
+                     g.threads, g.pmax_cap);
+      }
+      g.smem = std::max(g.smem, s);
+    }
+    hp.groups.push_back(g);
+  }
+  return LP_OK;
+}
+
+struct HistDev {
+  const PairDesc* pairs;
+  const EntryDesc* entries;
+  const DrawConst* draws;
+  const uint64_t* binom;
+  const WorkItem* work;
+  uint32_t* evt;
+  uint32_t* h0;
+  uint32_t* hist;
+};
+
+cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int* launches) {
+  cudaError_t e;
+  if (hp.evt_len > 0) {
+    e = cudaMemsetAsync(d.evt, 0, sizeof(uint32_t) * hp.evt_len, st);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemsetAsync(d.h0, 0, sizeof(uint32_t) * std::max<int64_t>(hp.h0_len, 1), st);
+  if (e != cudaSuccess) return e;
+  for (const Group& g : hp.groups) {
+    const WorkItem* w = d.work + g.first;
+    if (g.kind == 0)
+      e = launch_hist_regs(g.kmax, g.smem_evt, g.count, g.smem, st, w, d.pairs, d.entries, d.draws,
+                           d.binom, d.evt, d.h0);
+    else
+      e = launch_hist_ctr(g.smem_evt, g.count, g.threads, g.smem, g.pmax_cap, st, w, d.pairs,
+                          d.entries, d.draws, d.binom, d.evt, d.h0);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+  }
+  e = launch_finalize((int)hp.pairs.size(), (int)hp.entries.size(), st, d.pairs, d.entries, d.evt,
+                      d.h0, d.hist);
+  if (!hp.pairs.empty()) *launches += 2;
+  return e;
+}
+
+// thr(D, P) rows for the depths a plan touches
+struct ThrTable {
+  std::vector<int32_t> row;   // by P: offset, -1 if absent
+  std::vector<double> vals;
+};
+
+void build_thr(Model& m, const std::map<int, int>& need, int pmax, ThrTable& t) {
+  t.row.assign(pmax + 2, -1);
+  t.vals.clear();
+  for (const auto& [P, Dm] : need) {
+    t.row[P] = (int32_t)t.vals.size();
+    for (int D = 0; D <= Dm; ++D) t.vals.push_back(D == 0 ? 0.0 : m.rate(D, P));
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// NCCL is bound at run time (dlopen) so this library never drags a second
+// libnccl.so.2 into a process that also loads torch's bundled NCCL.
+// LIVEPUT_NCCL_LIB may name the library; default "libnccl.so.2" (which
+// resolves to the already-loaded copy when torch was imported first).
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    const char* env = getenv("LIVEPUT_NCCL_LIB");
+    void* so = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!so) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(so, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(so, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(so, "ncclCommDestroy");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(so, "ncclAllReduce");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(so, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+}  // namespace
+}  // namespace lp
+
+using namespace lp;
+
+// ---------------------------------------------------------------------------
+struct lp_handle {
+  Model model;
+  lp_costs costs{};
+  lp_options opt{};
+  CostScalars cs{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::string err;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // re-plan state
+  bool prepared = false;
+  int horizon = 0;
+  HistPlan hp;
+  std::vector<LevelDesc> levels;
+  std::vector<NodeCfg> cfg;
+  std::vector<NodeCost> cost;
+  std::vector<int4> lrows;
+  ThrTable thr;
+  DpScalars S{};
+  size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
+         off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
+  size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
+         w_plan = 0, w_live = 0, w_final = 0;
+  DevBuf tables, work;
+  PinBuf pin_up, pin_down;
+  size_t up_bytes = 0;
+  lp_stats stats{};
+
+  // ensemble calls (phi / survivor_hist / liveput) and their cache
+  DevBuf e_tables, e_work;
+  std::map<std::tuple<int, int, int>, std::pair<int, std::vector<uint32_t>>> hist_cache;
+};
+
+namespace {
+
+lp_status fail(lp_handle* h, lp_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  else g_global_err = buf;
+  return s;
+}
+
+#define LP_CUDA(h, call)                                                               \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return fail((h), LP_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                           \
+  } while (0)
+
+template <typename T>
+T* dptr(DevBuf& b, size_t off) {
+  return reinterpret_cast<T*>(static_cast<unsigned char*>(b.p) + off);
+}
+
+// Builds and uploads a hist plan into (tables, work); returns device ptrs.
+lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& work, HistDev& d,
+                      Packer& pk, std::vector<size_t>& extra_offs) {
+  (void)extra_offs;
+  const size_t op = pk.add(hp.pairs), oe = pk.add(hp.entries), od = pk.add(hp.draws),
+               ob = pk.add(hp.binom), ow = pk.add(hp.work);
+  LP_CUDA(h, tables.ensure(pk.bytes.size()));
+  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
+  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
+  LP_CUDA(h, cudaMemcpyAsync(tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
+                             h->stream));
+  const size_t wb = a16(4 * std::max<int64_t>(hp.evt_len, 1)) + a16(4 * std::max<int64_t>(hp.h0_len, 1)) +
+                    a16(4 * std::max<int64_t>(hp.hist_len, 1));
+  LP_CUDA(h, work.ensure(wb));
+  d.pairs = dptr<PairDesc>(tables, op);
+  d.entries = dptr<EntryDesc>(tables, oe);
+  d.draws = dptr<DrawConst>(tables, od);
+  d.binom = dptr<uint64_t>(tables, ob);
+  d.work = dptr<WorkItem>(tables, ow);
+  d.evt = dptr<uint32_t>(work, 0);
+  d.h0 = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)));
+  d.hist = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)) +
+                                    a16(4 * std::max<int64_t>(hp.h0_len, 1)));
+  return LP_OK;
+}
+
+// Planner ensemble semantics (optimizer.cpp:64-94).
+lp_status planner_spec(lp_handle* h, int n, int k, EnsembleSpec& sp) {
+  if (k < 0 || k > n) return fail(h, LP_EINVAL, "sample_vectors: bad n_minus");
+  sp.n = n;
+  sp.k = k;
+  const uint64_t cnt = scenario_count(n, k);
+  sp.exact = cnt <= h->opt.exact_cap;
+  if (sp.exact) {
+    if (cnt > kEnumerationCap)
+      return fail(h, LP_EINVAL, "enumerate_vectors: scenario space too large, sample instead");
+    sp.count = cnt;
+  } else {
+    if (h->opt.mc_trials < 1) return fail(h, LP_EINVAL, "sample_vectors: trials must be >= 1");
+    sp.count = (uint64_t)h->opt.mc_trials;
+  }
+  sp.seed = mix_seed(mix_seed(h->opt.mc_seed, (uint64_t)n), (uint64_t)k);
+  return LP_OK;
+}
+
+// Runs one ensemble (single GPU) for the entries of `sp` and returns the
+// u32 histogram rows of (D, P) in `rows` (d = 0..min(k, D)).
+lp_status ensemble_rows(lp_handle* h, const EnsembleSpec& sp, int D, int P,
+                        std::vector<uint32_t>& rows) {
+  HistPlan hp;
+  std::string err;
+  lp_status s = build_hist_plan({sp}, 0, 1, hp, err);
+  if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+  Packer pk;
+  HistDev d{};
+  std::vector<size_t> extra;
+  s = upload_hist(h, hp, h->e_tables, h->e_work, d, pk, extra);
+  if (s != LP_OK) return s;
+  int launches = 0;
+  LP_CUDA(h, run_hist(hp, d, h->stream, &launches));
+  // locate (D, P)
+  int e = -1;
+  for (size_t i = 0; i < hp.entries.size(); ++i)
+    if (hp.entries[i].P == P) e = (int)i;
+  if (e < 0 || D > hp.entries[e].Dmax) return fail(h, LP_EINVAL, "internal: entry missing");
+  const int off = hp.entries[e].hist_off + hist_row(D, sp.k);
+  const int len = std::min(sp.k, D) + 1;
+  rows.assign(len, 0);
+  LP_CUDA(h, h->pin_down.ensure(sizeof(uint32_t) * len));
+  LP_CUDA(h, cudaMemcpyAsync(h->pin_down.p, d.hist + off, sizeof(uint32_t) * len,
+                             cudaMemcpyDeviceToHost, h->stream));
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  std::memcpy(rows.data(), h->pin_down.p, sizeof(uint32_t) * len);
+  return LP_OK;
+}
+
+// Cached planner histogram of (D, P) at (n, k): the reference's hist_cache_
+// (optimizer.hpp:88) keyed by (n, k, P) with the largest D computed.
+lp_status planner_rows(lp_handle* h, int D, int P, int n, int k, std::vector<uint32_t>& rows,
+                       uint64_t* total) {
+  EnsembleSpec sp;
+  lp_status s = planner_spec(h, n, k, sp);
+  if (s != LP_OK) return s;
+  *total = sp.count;
+  auto key = std::make_tuple(n, k, P);
+  auto it = h->hist_cache.find(key);
+  if (it == h->hist_cache.end() || it->second.first < D) {
+    const int Dm = n / P;  // every D of this depth at once
+    sp.dmax_by_p[P] = std::max(Dm, D);
+    std::vector<uint32_t> all;
+    // fetch all rows of the entry: run and copy D = 1..Dm
+    HistPlan hp;
+    std::string err;
+    s = build_hist_plan({sp}, 0, 1, hp, err);
+    if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+    Packer pk;
+    HistDev d{};
+    std::vector<size_t> extra;
+    s = upload_hist(h, hp, h->e_tables, h->e_work, d, pk, extra);
+    if (s != LP_OK) return s;
+    int launches = 0;
+    LP_CUDA(h, run_hist(hp, d, h->stream, &launches));
+    const size_t len = (size_t)hp.hist_len;
+    LP_CUDA(h, h->pin_down.ensure(sizeof(uint32_t) * len));
+    LP_CUDA(h, cudaMemcpyAsync(h->pin_down.p, d.hist, sizeof(uint32_t) * len,
+                               cudaMemcpyDeviceToHost, h->stream));
+    LP_CUDA(h, cudaStreamSynchronize(h->stream));
+    all.assign(static_cast<uint32_t*>(h->pin_down.p), static_cast<uint32_t*>(h->pin_down.p) + len);
+    h->hist_cache[key] = {sp.dmax_by_p[P], std::move(all)};
+    it = h->hist_cache.find(key);
+  }
+  const int off = hist_row(D, k);
+  const int len = std::min(k, D) + 1;
+  rows.assign(it->second.second.begin() + off, it->second.second.begin() + off + len);
+  return LP_OK;
+}
+
+NodeCost node_cost(lp_handle* h, int d, int p) {
+  NodeCost c{};
+  if (d <= 0) return c;
+  c.thr = h->model.rate(d, p);
+  c.pipe = h->model.pipe_transfer(p);
+  c.unit = h->model.inter_unit(p);
+  // resume_cost (migration.cpp:100-104)
+  c.resume = h->cs.fresh_fixed + h->cs.build + h->cs.update + c.pipe;
+  return c;
+}
+
+DpScalars dp_scalars(lp_handle* h, int horizon) {
+  DpScalars S{};
+  S.T = h->opt.interval_s;
+  S.build = h->cs.build;
+  S.update = h->cs.update;
+  S.rollback = h->opt.rollback_penalty_s;
+  S.fresh_fixed = h->cs.fresh_fixed;
+  S.strict = h->opt.strict_conditional;
+  S.horizon = horizon;
+  return S;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* lp_last_global_error(void) { return g_global_err.c_str(); }
+const char* lp_last_error(const lp_handle* h) { return h ? h->err.c_str() : g_global_err.c_str(); }
+
+int32_t lp_max_instances(void) { return kMaxN; }
+
+const char* lp_build_info(void) {
+  return "liveput sm_100a (tcgen05-free integer/FP64 path); kMaxN=2048; variants R(k<=16) C(k<=255)";
+}
+
+lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_options* options,
+                    int32_t device, lp_handle** out) {
+  if (!profile || !costs || !options || !out)
+    return fail(nullptr, LP_EINVAL, "lp_create: null argument");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, LP_ECUDA, "lp_create: no CUDA device (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(nullptr, LP_EINVAL, "lp_create: bad device %d", device);
+  lp_handle* h = new lp_handle();
+  h->model = Model(*profile);
+  h->costs = *costs;
+  h->opt = *options;
+  h->cs = cost_scalars(*costs);
+  h->device = device;
+  if ((e = cudaSetDevice(device)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    delete h;
+    return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
+  }
+  for (auto& ev : h->ev) cudaEventCreate(&ev);
+  *out = h;
+  return LP_OK;
+}
+
+void lp_destroy(lp_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  for (auto& ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+lp_status lp_get_options(const lp_handle* h, lp_options* out) {
+  if (!h || !out) return fail(nullptr, LP_EINVAL, "null argument");
+  *out = h->opt;
+  return LP_OK;
+}
+
+void* lp_stream(lp_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+// ---------------------------------------------------------------------------
+// prepare: levels (optimizer.cpp:148-183), ensembles, tables; one H2D copy.
+lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len) {
+  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  if (!n_seq || len < 2) return fail(h, LP_EINVAL, "dp_optimize: need at least N_i and N_{i+1}");
+  cudaSetDevice(h->device);
+  for (int i = 0; i < len; ++i) {
+    if (n_seq[i] < 0) return fail(h, LP_EINVAL, "dp_optimize: negative availability");
+    if (n_seq[i] > kMaxN)
+      return fail(h, LP_EUNSUPPORTED, "dp_optimize: n=%d exceeds supported maximum %d", n_seq[i], kMaxN);
+  }
+  const bool cur_on = current.pipelines > 0;
+  if (cur_on) {
+    if (current.stages < 1) return fail(h, LP_EINVAL, "dp_optimize: current config has no stages");
+    if ((long long)current.pipelines * current.stages > n_seq[0])
+      // the reference reads past the preemption vector here (preemption.cpp:63)
+      return fail(h, LP_EINVAL, "dp_optimize: current config exceeds n_seq[0]");
+  }
+  const int H = len - 1;
+  h->horizon = H;
+  h->levels.assign(H, LevelDesc{});
+  h->cfg.clear();
+  h->cost.clear();
+  std::vector<int> lbase(H + 1), lcount(H + 1);
+  // level 0: current
+  lbase[0] = 0;
+  lcount[0] = 1;
+  h->cfg.push_back({cur_on ? current.pipelines : 0, cur_on ? current.stages : 0, -1, 0});
+  h->cost.push_back(NodeCost{});
+  for (int j = 1; j <= H; ++j) {
+    lbase[j] = (int)h->cfg.size();
+    for (const Cfg& c : h->model.configs(n_seq[j])) {
+      h->cfg.push_back({c.d, c.p, -1, 0});
+      h->cost.push_back(node_cost(h, c.d, c.p));
+    }
+    h->cfg.push_back({0, 0, -1, 0});  // suspension is always reachable
+    h->cost.push_back(NodeCost{});
+    lcount[j] = (int)h->cfg.size() - lbase[j];
+  }
+  // ensembles: one per distinct (n_now, k) whose histograms phi will read
+  std::map<std::pair<int, int>, int> spec_of;
+  std::vector<EnsembleSpec> specs;
+  std::vector<int> level_spec(H, -1);
+  std::map<std::tuple<int, int, int, int>, char> keys;  // reference hist keys (D,P,n,k)
+  for (int j = 0; j < H; ++j) {
+    const int n_now = n_seq[j], n_next = n_seq[j + 1];
+    const int k = std::max(0, n_now - n_next);
+    bool any_prev = false;
+    for (int i = 0; i < lcount[j]; ++i) any_prev |= h->cfg[lbase[j] + i].d > 0;
+    const bool any_next = !h->model.configs(n_next).empty();
+    if (!any_prev || !any_next) continue;
+    auto key = std::make_pair(n_now, k);
+    auto it = spec_of.find(key);
+    if (it == spec_of.end()) {
+      EnsembleSpec sp;
+      lp_status s = planner_spec(h, n_now, k, sp);
+      if (s != LP_OK) return s;
+      it = spec_of.emplace(key, (int)specs.size()).first;
+      specs.push_back(sp);
+    }
+    EnsembleSpec& sp = specs[it->second];
+    for (int i = 0; i < lcount[j]; ++i) {
+      const NodeCfg& c = h->cfg[lbase[j] + i];
+      if (c.d <= 0) continue;
+      int& dm = sp.dmax_by_p[c.p];
+      dm = std::max(dm, j == 0 ? c.d : n_now / c.p);
+      keys[{c.d, c.p, n_now, k}] = 1;
+    }
+    level_spec[j] = it->second;
+  }
+  for (const auto& [kk, v] : keys) {
+    (void)v;
+    specs[spec_of[{std::get<2>(kk), std::get<3>(kk)}]].ref_keys++;
+  }
+  std::string err;
+  lp_status s = build_hist_plan(specs, h->rank, h->nranks, h->hp, err);
+  if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+  // node histogram rows + levels
+  std::map<int, int> thr_need;
+  int pmax = 1;
+  for (int j = 0; j < H; ++j) {
+    LevelDesc& L = h->levels[j];
+    L.n_now = n_seq[j];
+    L.n_next = n_seq[j + 1];
+    L.k = std::max(0, L.n_now - L.n_next);
+    L.prev_base = lbase[j];
+    L.prev_count = lcount[j];
+    L.next_base = lbase[j + 1];
+    L.next_count = lcount[j + 1];
+    L.fresh = L.n_next > L.n_now ? 1 : 0;
+    L.fixed = L.fresh ? h->cs.fresh_fixed : 0.0;
+    L.has_hist = level_spec[j] >= 0;
+    if (!L.has_hist) continue;
+    const PairDesc& pd = h->hp.pairs[level_spec[j]];
+    L.total = pd.count;
+    for (int i = 0; i < lcount[j]; ++i) {
+      NodeCfg& c = h->cfg[lbase[j] + i];
+      if (c.d <= 0) continue;
+      for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
+        if (h->hp.entries[e].P == c.p) c.hist_off = h->hp.entries[e].hist_off + hist_row(c.d, L.k);
+      int& dm = thr_need[c.p];
+      dm = std::max(dm, c.d);
+      pmax = std::max(pmax, c.p);
+    }
+  }
+  if (h->opt.strict_conditional)
+    for (int j = 1; j <= H; ++j)
+      for (int i = 0; i < lcount[j]; ++i) {
+        const NodeCfg& c = h->cfg[lbase[j] + i];
+        if (c.d <= 0) continue;
+        int& dm = thr_need[c.p];
+        dm = std::max(dm, c.d);
+        pmax = std::max(pmax, c.p);
+      }
+  build_thr(h->model, thr_need, pmax, h->thr);
+  // liveput rows
+  h->lrows.clear();
+  for (int j = 0; j < H; ++j) {
+    if (!h->levels[j].has_hist) continue;
+    for (int i = 0; i < lcount[j]; ++i) {
+      const int gi = lbase[j] + i;
+      if (h->cfg[gi].d > 0 && h->cfg[gi].hist_off >= 0)
+        h->lrows.push_back(make_int4(j, gi, (int)h->lrows.size(), 0));
+    }
+  }
+  h->S = dp_scalars(h, H);
+  // ---- pack + upload
+  Packer pk;
+  h->off_pairs = pk.add(h->hp.pairs);
+  h->off_entries = pk.add(h->hp.entries);
+  h->off_draws = pk.add(h->hp.draws);
+  h->off_binom = pk.add(h->hp.binom);
+  h->off_work = pk.add(h->hp.work);
+  h->off_levels = pk.add(h->levels);
+  h->off_cfg = pk.add(h->cfg);
+  h->off_cost = pk.add(h->cost);
+  h->off_lrows = pk.add(h->lrows);
+  h->off_thr = pk.add(h->thr.vals);
+  h->off_throw = pk.add(h->thr.row);
+  LP_CUDA(h, h->tables.ensure(pk.bytes.size()));
+  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
+  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
+  LP_CUDA(h, cudaMemcpyAsync(h->tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
+                             h->stream));
+  h->up_bytes = pk.bytes.size();
+  // work arena
+  const size_t nn = h->cfg.size();
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
+  h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
+  h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
+  h->w_val = take(8 * nn);
+  h->w_mig = take(8 * nn);
+  h->w_par = take(4 * nn);
+  h->w_stc = take(8 * nn);
+  h->w_stm = take(8 * nn);
+  h->w_plan = take(sizeof(lp_plan_step) * H);
+  h->w_live = take(sizeof(lp_liveput_row) * std::max<size_t>(h->lrows.size(), 1));
+  h->w_final = take(8);
+  LP_CUDA(h, h->work.ensure(o));
+  h->prepared = true;
+  std::memset(&h->stats, 0, sizeof h->stats);
+  h->stats.resolutions = h->hp.resolutions;
+  h->stats.scenarios = h->hp.scenarios;
+  h->stats.local_scenarios = h->hp.local_scenarios;
+  h->stats.mc_pairs = h->hp.mc_pairs;
+  h->stats.exact_pairs = h->hp.exact_pairs;
+  h->stats.horizon = H;
+  h->stats.hist_alg_ops = h->hp.alg_ops;
+  h->stats.h2d_bytes = pk.bytes.size() + sizeof(int32_t) * len;
+  return LP_OK;
+}
+
+lp_status lp_execute(lp_handle* h) {
+  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  if (!h->prepared) return fail(h, LP_EINVAL, "lp_execute: call lp_prepare first");
+  cudaSetDevice(h->device);
+  cudaStream_t st = h->stream;
+  HistDev d{};
+  d.pairs = dptr<PairDesc>(h->tables, h->off_pairs);
+  d.entries = dptr<EntryDesc>(h->tables, h->off_entries);
+  d.draws = dptr<DrawConst>(h->tables, h->off_draws);
+  d.binom = dptr<uint64_t>(h->tables, h->off_binom);
+  d.work = dptr<WorkItem>(h->tables, h->off_work);
+  d.evt = dptr<uint32_t>(h->work, h->w_evt);
+  d.h0 = dptr<uint32_t>(h->work, h->w_h0);
+  d.hist = dptr<uint32_t>(h->work, h->w_hist);
+  int launches = 0;
+  LP_CUDA(h, cudaEventRecord(h->ev[0], st));
+  LP_CUDA(h, run_hist(h->hp, d, st, &launches));
+  LP_CUDA(h, cudaEventRecord(h->ev[1], st));
+  if (h->nranks > 1 && h->hp.hist_len > 0) {
+    ncclResult_t r = nccl().AllReduce(d.hist, d.hist, (size_t)h->hp.hist_len, ncclUint32, ncclSum,
+                                      h->comm, st);
+    if (r != ncclSuccess) return fail(h, LP_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(r));
+  }
+  LP_CUDA(h, cudaEventRecord(h->ev[2], st));
+  const LevelDesc* lv = dptr<LevelDesc>(h->tables, h->off_levels);
+  const NodeCfg* cfg = dptr<NodeCfg>(h->tables, h->off_cfg);
+  const NodeCost* cost = dptr<NodeCost>(h->tables, h->off_cost);
+  const double* thr = dptr<double>(h->tables, h->off_thr);
+  const int32_t* throw_ = dptr<int32_t>(h->tables, h->off_throw);
+  double* val = dptr<double>(h->work, h->w_val);
+  double* mig = dptr<double>(h->work, h->w_mig);
+  int32_t* par = dptr<int32_t>(h->work, h->w_par);
+  double* stc = dptr<double>(h->work, h->w_stc);
+  double* stm = dptr<double>(h->work, h->w_stm);
+  LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
+  LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
+  for (int j = 0; j < h->horizon; ++j) {
+    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, cost, d.hist, thr, throw_,
+                              h->S, val, mig, par, stc, stm));
+    ++launches;
+  }
+  LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
+                             dptr<lp_plan_step>(h->work, h->w_plan),
+                             dptr<double>(h->work, h->w_final)));
+  ++launches;
+  if (!h->lrows.empty()) {
+    LP_CUDA(h, launch_liveput((int)h->lrows.size(), st, dptr<int4>(h->tables, h->off_lrows), lv,
+                              cfg, d.hist, thr, throw_, dptr<lp_liveput_row>(h->work, h->w_live)));
+    ++launches;
+  }
+  LP_CUDA(h, cudaEventRecord(h->ev[3], st));
+  h->stats.kernel_launches = launches;
+  return LP_OK;
+}
+
+lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_t cap,
+                   int32_t* rows) {
+  if (!h || !out) return fail(h, LP_EINVAL, "lp_fetch: null argument");
+  if (!h->prepared) return fail(h, LP_EINVAL, "lp_fetch: nothing prepared");
+  cudaSetDevice(h->device);
+  const size_t plan_b = sizeof(lp_plan_step) * h->horizon;
+  const size_t nl = live ? std::min<size_t>(h->lrows.size(), (size_t)std::max(cap, 0)) : 0;
+  const size_t live_b = sizeof(lp_liveput_row) * nl;
+  LP_CUDA(h, h->pin_down.ensure(plan_b + live_b + 64));
+  unsigned char* pd = static_cast<unsigned char*>(h->pin_down.p);
+  LP_CUDA(h, cudaMemcpyAsync(pd, dptr<void>(h->work, h->w_plan), plan_b, cudaMemcpyDeviceToHost,
+                             h->stream));
+  if (live_b)
+    LP_CUDA(h, cudaMemcpyAsync(pd + plan_b, dptr<void>(h->work, h->w_live), live_b,
+                               cudaMemcpyDeviceToHost, h->stream));
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  std::memcpy(out, pd, plan_b);
+  if (live_b) std::memcpy(live, pd + plan_b, live_b);
+  if (rows) *rows = (int32_t)h->lrows.size();
+  h->stats.d2h_bytes = plan_b + live_b;
+  return LP_OK;
+}
+
+lp_status lp_replan(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len,
+                    lp_plan_step* out, lp_liveput_row* live, int32_t cap, int32_t* rows) {
+  lp_status s = lp_prepare(h, current, n_seq, len);
+  if (s != LP_OK) return s;
+  s = lp_execute(h);
+  if (s != LP_OK) return s;
+  return lp_fetch(h, out, live, cap, rows);
+}
+
+lp_status lp_get_stats(const lp_handle* hc, lp_stats* out) {
+  lp_handle* h = const_cast<lp_handle*>(hc);
+  if (!h || !out) return fail(h, LP_EINVAL, "null argument");
+  if (h->prepared && h->stats.kernel_launches > 0) {
+    cudaSetDevice(h->device);
+    LP_CUDA(h, cudaStreamSynchronize(h->stream));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);
+    cudaEventElapsedTime(&b, h->ev[1], h->ev[2]);
+    cudaEventElapsedTime(&c, h->ev[2], h->ev[3]);
+    h->stats.hist_ms = a;
+    h->stats.reduce_ms = b;
+    h->stats.dp_ms = c;
+    h->stats.total_ms = (double)a + b + c;
+  }
+  *out = h->stats;
+  return LP_OK;
+}
+
+// ---------------------------------------------------------------------------
+lp_status lp_phi(lp_handle* h, lp_config prev, lp_config next, int32_t n_now, int32_t n_next,
+                 double* committed, double* mig) {
+  if (!h || !committed || !mig) return fail(h, LP_EINVAL, "lp_phi: null argument");
+  cudaSetDevice(h->device);
+  NodeCfg pv{prev.pipelines > 0 ? prev.pipelines : 0, prev.pipelines > 0 ? prev.stages : 0, 0, 0};
+  NodeCfg nx{next.pipelines > 0 ? next.pipelines : 0, next.pipelines > 0 ? next.stages : 0, 0, 0};
+  // optimizer.cpp:99-101: suspended / infeasible / oversized next -> {0, 0}
+  if (nx.d <= 0 || !h->model.depth_ok(nx.p) || (long long)nx.d * nx.p > n_next) {
+    *committed = 0.0;
+    *mig = 0.0;
+    return LP_OK;
+  }
+  LevelDesc L{};
+  L.n_now = n_now;
+  L.n_next = n_next;
+  L.k = std::max(0, n_now - n_next);
+  L.fresh = n_next > n_now;
+  L.fixed = L.fresh ? h->cs.fresh_fixed : 0.0;
+  std::vector<uint32_t> rows(1, 0);
+  if (pv.d > 0) {
+    if (pv.p < 1 || (long long)pv.d * pv.p > n_now)
+      return fail(h, LP_EINVAL, "phi: prev config exceeds n_now");
+    uint64_t total = 0;
+    lp_status s = planner_rows(h, pv.d, pv.p, n_now, L.k, rows, &total);
+    if (s != LP_OK) return s;
+    L.total = total;
+  }
+  std::map<int, int> need;
+  need[nx.p] = nx.d;
+  ThrTable t;
+  build_thr(h->model, need, nx.p, t);
+  Packer pk;
+  const size_t oh = pk.add(rows), ot = pk.add(t.vals), orow = pk.add(t.row);
+  const size_t oout = pk.add(nullptr, 16);
+  LP_CUDA(h, h->e_tables.ensure(pk.bytes.size()));
+  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
+  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
+  LP_CUDA(h, cudaMemcpyAsync(h->e_tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
+                             h->stream));
+  pv.hist_off = 0;
+  const NodeCost nc = node_cost(h, nx.d, nx.p);
+  const DpScalars S = dp_scalars(h, 1);
+  LP_CUDA(h, launch_phi_single(pv, nx, nc, L, S, dptr<uint32_t>(h->e_tables, oh),
+                               dptr<double>(h->e_tables, ot), dptr<int32_t>(h->e_tables, orow),
+                               dptr<double>(h->e_tables, oout), h->stream));
+  LP_CUDA(h, h->pin_down.ensure(16));
+  LP_CUDA(h, cudaMemcpyAsync(h->pin_down.p, dptr<double>(h->e_tables, oout), 16,
+                             cudaMemcpyDeviceToHost, h->stream));
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  const double* r = static_cast<const double*>(h->pin_down.p);
+  *committed = r[0];
+  *mig = r[1];
+  return LP_OK;
+}
+
+lp_status lp_sequence_value(lp_handle* h, lp_config current, const lp_config* seq,
+                            const int32_t* n_seq, int32_t len, double* out) {
+  if (!h || !out || !n_seq) return fail(h, LP_EINVAL, "null argument");
+  if (len < 1 || (len > 1 && !seq))
+    return fail(h, LP_EINVAL, "sequence_value: sequence/N length mismatch");
+  double value = 0.0;
+  lp_config prev = current;
+  for (int j = 0; j + 1 < len; ++j) {
+    double c = 0, m = 0;
+    lp_status s = lp_phi(h, prev, seq[j], n_seq[j], n_seq[j + 1], &c, &m);
+    if (s != LP_OK) return s;
+    value += c;
+    prev = seq[j];
+  }
+  *out = value;
+  return LP_OK;
+}
+
+lp_status lp_survivor_hist(lp_handle* h, lp_config prev, int32_t n_now, int32_t n_minus,
+                           uint64_t* counts, uint64_t* total) {
+  if (!h || !counts || !total) return fail(h, LP_EINVAL, "null argument");
+  if (prev.pipelines < 1 || prev.stages < 1 || (long long)prev.pipelines * prev.stages > n_now)
+    return fail(h, LP_EINVAL, "survivor_hist: config exceeds n_now");
+  cudaSetDevice(h->device);
+  std::vector<uint32_t> rows;
+  lp_status s = planner_rows(h, prev.pipelines, prev.stages, n_now, n_minus, rows, total);
+  if (s != LP_OK) return s;
+  for (int m = 0; m <= prev.pipelines; ++m) counts[m] = 0;
+  for (size_t d = 0; d < rows.size(); ++d) counts[prev.pipelines - (int)d] = rows[d];
+  return LP_OK;
+}
+
+lp_status lp_expected_liveput(lp_handle* h, lp_config cfg, int32_t n, int32_t n_minus,
+                              int32_t exact, int32_t trials, uint64_t seed, double* out) {
+  if (!h || !out) return fail(h, LP_EINVAL, "null argument");
+  if ((long long)cfg.pipelines * cfg.stages > n)
+    return fail(h, LP_EINVAL, "expected_liveput: config exceeds n");
+  if (n_minus < 0 || n_minus > n) return fail(h, LP_EINVAL, "sample_vectors: bad n_minus");
+  if (cfg.pipelines < 1 || cfg.stages < 1) return fail(h, LP_EINVAL, "expected_liveput: empty config");
+  cudaSetDevice(h->device);
+  EnsembleSpec sp;
+  sp.n = n;
+  sp.k = n_minus;
+  sp.exact = exact != 0;
+  if (sp.exact) {
+    sp.count = scenario_count(n, n_minus);
+    if (sp.count > kEnumerationCap)
+      return fail(h, LP_EINVAL, "enumerate_vectors: scenario space too large, sample instead");
+  } else {
+    if (trials < 1) return fail(h, LP_EINVAL, "sample_vectors: trials must be >= 1");
+    sp.count = (uint64_t)trials;
+  }
+  sp.seed = seed;
+  sp.dmax_by_p[cfg.stages] = cfg.pipelines;
+  std::vector<uint32_t> rows;
+  lp_status s = ensemble_rows(h, sp, cfg.pipelines, cfg.stages, rows);
+  if (s != LP_OK) return s;
+  // device liveput of the single row
+  std::map<int, int> need;
+  need[cfg.stages] = cfg.pipelines;
+  ThrTable t;
+  build_thr(h->model, need, cfg.stages, t);
+  LevelDesc L{};
+  L.k = n_minus;
+  L.total = sp.count;
+  NodeCfg c{cfg.pipelines, cfg.stages, 0, 0};
+  int4 row = make_int4(0, 0, 0, 0);
+  Packer pk;
+  const size_t oh = pk.add(rows), ot = pk.add(t.vals), orow = pk.add(t.row);
+  const size_t ol = pk.add(&L, sizeof L), oc = pk.add(&c, sizeof c), orw = pk.add(&row, sizeof row);
+  const size_t oout = pk.add(nullptr, sizeof(lp_liveput_row));
+  LP_CUDA(h, h->e_tables.ensure(pk.bytes.size()));
+  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
+  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
+  LP_CUDA(h, cudaMemcpyAsync(h->e_tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
+                             h->stream));
+  LP_CUDA(h, launch_liveput(1, h->stream, dptr<int4>(h->e_tables, orw),
+                            dptr<LevelDesc>(h->e_tables, ol), dptr<NodeCfg>(h->e_tables, oc),
+                            dptr<uint32_t>(h->e_tables, oh), dptr<double>(h->e_tables, ot),
+                            dptr<int32_t>(h->e_tables, orow),
+                            dptr<lp_liveput_row>(h->e_tables, oout)));
+  LP_CUDA(h, h->pin_down.ensure(sizeof(lp_liveput_row)));
+  LP_CUDA(h, cudaMemcpyAsync(h->pin_down.p, dptr<void>(h->e_tables, oout), sizeof(lp_liveput_row),
+                             cudaMemcpyDeviceToHost, h->stream));
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  *out = static_cast<lp_liveput_row*>(h->pin_down.p)->liveput;
+  return LP_OK;
+}
+
+static lp_status dump_common(lp_handle* h, int32_t n, int32_t k, int32_t exact, int32_t trials,
+                             uint64_t seed, const lp_config* cfgs, int32_t n_cfg,
+                             uint16_t* sorted_out, uint16_t* m_out) {
+  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  if (k < 0 || k > n) return fail(h, LP_EINVAL, "sample_vectors: bad n_minus");
+  if (n > kMaxN) return fail(h, LP_EUNSUPPORTED, "n exceeds supported maximum");
+  if (trials < 1) return fail(h, LP_EINVAL, "sample_vectors: trials must be >= 1");
+  if (exact && (uint64_t)trials != scenario_count(n, k))
+    return fail(h, LP_EINVAL, "dump: exact mode needs trials == C(n, k)");
+  for (int c = 0; c < n_cfg; ++c)
+    if (cfgs[c].pipelines < 1 || cfgs[c].stages < 1 ||
+        (long long)cfgs[c].pipelines * cfgs[c].stages > n)
+      return fail(h, LP_EINVAL, "dump: config exceeds n");
+  cudaSetDevice(h->device);
+  EnsembleSpec sp;
+  sp.n = n;
+  sp.k = k;
+  sp.exact = exact != 0;
+  sp.count = (uint64_t)trials;
+  sp.seed = seed;
+  HistPlan hp;
+  std::string err;
+  lp_status s = build_hist_plan({sp}, 0, 1, hp, err);
+  if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+  std::vector<int2> cv(std::max(n_cfg, 1));
+  for (int c = 0; c < n_cfg; ++c) cv[c] = make_int2(cfgs[c].pipelines, cfgs[c].stages);
+  Packer pk;
+  const size_t od = pk.add(hp.draws), ob = pk.add(hp.binom), oc = pk.add(cv);
+  LP_CUDA(h, h->e_tables.ensure(pk.bytes.size()));
+  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
+  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
+  LP_CUDA(h, cudaMemcpyAsync(h->e_tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
+                             h->stream));
+  const size_t kk = std::max(k, 1);
+  const size_t nw = (n + 31) / 32;
+  const size_t srt_b = 2 * kk * trials, m_b = m_out ? 2 * (size_t)trials * std::max(n_cfg, 1) : 0;
+  const size_t scr_b = k > 16 ? 4 * (size_t)(k + nw) * trials : 4;
+  const size_t o1 = 0, o2 = (srt_b + 255) & ~size_t(255), o3 = o2 + ((m_b + 255) & ~size_t(255));
+  LP_CUDA(h, h->e_work.ensure(o3 + scr_b));
+  const int stride = hp.pairs.empty() ? 1 : hp.pairs[0].binom_stride;
+  LP_CUDA(h, launch_dump(n, k, exact, trials, seed, dptr<DrawConst>(h->e_tables, od),
+                         dptr<uint64_t>(h->e_tables, ob), stride, dptr<uint32_t>(h->e_work, o3),
+                         dptr<uint16_t>(h->e_work, o1), dptr<int2>(h->e_tables, oc), n_cfg,
+                         m_out ? dptr<uint16_t>(h->e_work, o2) : nullptr, h->stream));
+  if (sorted_out)
+    LP_CUDA(h, cudaMemcpyAsync(sorted_out, dptr<uint16_t>(h->e_work, o1), 2 * (size_t)k * trials,
+                               cudaMemcpyDeviceToHost, h->stream));
+  if (m_out)
+    LP_CUDA(h, cudaMemcpyAsync(m_out, dptr<uint16_t>(h->e_work, o2), 2 * (size_t)trials * n_cfg,
+                               cudaMemcpyDeviceToHost, h->stream));
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  return LP_OK;
+}
+
+lp_status lp_dump_survivors(lp_handle* h, int32_t n, int32_t n_minus, int32_t exact, int32_t trials,
+                            uint64_t seed, const lp_config* cfgs, int32_t n_cfg, uint16_t* out) {
+  if (!out || !cfgs || n_cfg < 1) return fail(h, LP_EINVAL, "lp_dump_survivors: bad output");
+  return dump_common(h, n, n_minus, exact, trials, seed, cfgs, n_cfg, nullptr, out);
+}
+
+lp_status lp_dump_scenarios(lp_handle* h, int32_t n, int32_t n_minus, int32_t trials, uint64_t seed,
+                            uint16_t* out) {
+  if (!out) return fail(h, LP_EINVAL, "lp_dump_scenarios: null output");
+  if (n_minus == 0) return dump_common(h, n, 0, 0, trials, seed, nullptr, 0, nullptr, nullptr);
+  return dump_common(h, n, n_minus, 0, trials, seed, nullptr, 0, out, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+lp_status lp_nccl_unique_id(uint8_t out[LP_NCCL_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == LP_NCCL_ID_BYTES, "nccl id size");
+  if (!nccl().ok) return fail(nullptr, LP_ENCCL, "NCCL library could not be loaded");
+  ncclUniqueId id;
+  ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess)
+    return fail(nullptr, LP_ENCCL, "ncclGetUniqueId: %s", nccl().GetErrorString(r));
+  std::memcpy(out, &id, sizeof id);
+  return LP_OK;
+}
+
+lp_status lp_comm_init(lp_handle* h, const uint8_t id[LP_NCCL_ID_BYTES], int32_t nranks,
+                       int32_t rank) {
+  if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(h, LP_EINVAL, "lp_comm_init: bad argument");
+  cudaSetDevice(h->device);
+  if (h->comm) {
+    nccl().CommDestroy(h->comm);
+    h->comm = nullptr;
+  }
+  if (nranks > 1) {
+    if (!nccl().ok) return fail(h, LP_ENCCL, "NCCL library could not be loaded");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    ncclResult_t r = nccl().CommInitRank(&h->comm, nranks, uid, rank);
+    if (r != ncclSuccess)
+      return fail(h, LP_ENCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+  }
+  h->nranks = nranks;
+  h->rank = rank;
+  h->prepared = false;
+  return LP_OK;
+}
+
+// ---------------------------------------------------------------------------
+double lp_throughput(const lp_profile* p, lp_config c) { return Model(*p).rate(c.pipelines, c.stages); }
+
+int32_t lp_depth_feasible(const lp_profile* p, int32_t s) { return Model(*p).depth_ok(s) ? 1 : 0; }
+
+int32_t lp_enumerate_configs(const lp_profile* p, int32_t n, lp_config* out, int32_t cap) {
+  Model m(*p);
+  const auto& cs = m.configs(n);
+  for (int i = 0; i < (int)cs.size() && i < cap; ++i) out[i] = {cs[i].d, cs[i].p};
+  return (int32_t)cs.size();
+}
+
+int32_t lp_reactive_plan(const lp_profile* p, int32_t n, lp_config* out) {
+  Model m(*p);
+  Cfg c;
+  if (!m.reactive(n, &c)) return 0;
+  if (out) *out = {c.d, c.p};
+  return 1;
+}
+
+uint64_t lp_scenario_count(int32_t n, int32_t k) { return scenario_count(n, k); }
+uint64_t lp_mix_seed(uint64_t a, uint64_t b) { return mix_seed(a, b); }
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// lp_dp.cu — K2/K3/K4: transition value phi, the lookahead max-plus DP and
+// the on-device traceback (sm_100a, FP64).
+//
+// Replaces Planner::phi_uncached (optimizer.cpp:96-138) with
+// transition_outcome_min / resume_cost (migration.cpp:49-104), the level loop
+// of Planner::dp_optimize (optimizer.cpp:157-183), the final pick
+// (:185-195) and the traceback (:197-204).
+//
+// Bit-exactness: every FP64 operation is an explicit __d*_rn intrinsic in the
+// reference's operand order, so nothing is contracted into an FMA (the
+// reference's x86-64 build has no FMA).  Probabilities are
+// count_m / count exactly as the reference's normalised histogram.
+//
+// Layout: one warp per next-level node; lanes stride over prev nodes; the
+// (value desc, mig asc, first index) argmax is a warp shuffle reduction.  The
+// winning value, migration total, back-pointer and step terms of every node
+// stay in HBM for the traceback.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "liveput.h"
+#include "lp_layout.h"
+
+namespace lp {
+
+struct PhiOut {
+  double committed;
+  double mig;
+};
+
+__device__ __forceinline__ int replication_rounds(int sources, int transfers) {
+  int rounds = 0;
+  long long have = sources;
+  const long long need = static_cast<long long>(sources) + transfers;
+  while (have < need) {
+    have *= 2;
+    ++rounds;
+  }
+  return rounds;
+}
+
+// transition_outcome_min (migration.cpp:49-89) + rollback penalty
+// (optimizer.cpp:123).  fixed = fresh > 0 ? fresh_fixed : 0.0.
+__device__ __forceinline__ double transition_cost(int m, int sd, int sp, int td, int tp,
+                                                  double fixed, const NodeCost& nc,
+                                                  const DpScalars& S, bool* rollback) {
+  *rollback = false;
+  const double base = __dadd_rn(__dadd_rn(fixed, S.build), S.update);
+  if (m == 0) {
+    *rollback = true;
+    return __dadd_rn(base, nc.pipe);
+  }
+  if (tp != sp) return __dadd_rn(base, nc.pipe);
+  const int transfers = td - m > 0 ? td - m : 0;
+  const int rounds = replication_rounds(m, transfers);
+  const bool assigned_dead = m < sd;
+  if (rounds == 0 && !assigned_dead && td == sd) return 0.0;
+  if (rounds == 0) return base;
+  const double a = __dmul_rn(static_cast<double>(rounds), nc.unit);
+  const double inter = (nc.pipe < a) ? nc.pipe : a;  // std::min(a, pipe)
+  return __dadd_rn(base, inter);
+}
+
+// phi(prev, next, n_now, n_next) from the prev config's deficit histogram
+// (rows d = 0..min(k, D), m = D - d).  thr_tab/thr_row: throughput(D, P).
+__device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
+                                          const LevelDesc& L, const DpScalars& S,
+                                          const uint32_t* __restrict__ hist,
+                                          const double* __restrict__ thr_tab,
+                                          const int32_t* __restrict__ thr_row) {
+  PhiOut o{0.0, 0.0};
+  if (nx.d <= 0) return o;  // suspended next: nothing committed, nothing moved
+  if (pv.d <= 0) {          // resume from suspension (optimizer.cpp:108-115)
+    const double te = __dsub_rn(S.T, nc.resume);
+    o.mig = nc.resume;
+    o.committed = __dmul_rn(nc.thr, (0.0 < te) ? te : 0.0);
+    return o;
+  }
+  const uint32_t* h = hist + pv.hist_off;
+  const double total = static_cast<double>(L.total);
+  const int dmax = min(L.k, pv.d);
+  double committed = 0.0, cost_sum = 0.0;
+  for (int d = dmax; d >= 0; --d) {  // m = D - d ascending
+    const uint32_t cnt = h[d];
+    if (cnt == 0u) continue;
+    const int m = pv.d - d;
+    const double p = __ddiv_rn(static_cast<double>(cnt), total);
+    bool rb;
+    double cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
+    if (rb) cost = __dadd_rn(cost, S.rollback);
+    const double te = __dsub_rn(S.T, cost);
+    const double t_eff = (0.0 < te) ? te : 0.0;
+    double rate = nc.thr;
+    if (S.strict) {
+      const int alive = min(nx.d, m);
+      rate = alive > 0 ? thr_tab[thr_row[nx.p] + alive] : 0.0;
+    }
+    committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(p, rate), t_eff));
+    cost_sum = __dadd_rn(cost_sum, __dmul_rn(p, cost));
+  }
+  o.committed = committed;
+  o.mig = cost_sum;
+  return o;
+}
+
+struct Cand {
+  double value, mig, stc, stm;
+  int idx;
+};
+
+// a better than b in the DP's take order: value desc, mig asc, index asc.
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+  if (a.idx < 0) return false;
+  if (b.idx < 0) return true;
+  if (a.value > b.value) return true;
+  if (a.value < b.value) return false;
+  if (a.mig < b.mig) return true;
+  if (a.mig > b.mig) return false;
+  return a.idx < b.idx;
+}
+
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
+  Cand o;
+  o.value = __shfl_sync(0xffffffffu, c.value, src);
+  o.mig = __shfl_sync(0xffffffffu, c.mig, src);
+  o.stc = __shfl_sync(0xffffffffu, c.stc, src);
+  o.stm = __shfl_sync(0xffffffffu, c.stm, src);
+  o.idx = __shfl_sync(0xffffffffu, c.idx, src);
+  return o;
+}
+
+// F_{j+1}[c'] = max_c F_j[c] + phi(c, c') with the reference's tie rules.
+__global__ void __launch_bounds__(256) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
+                                                      const NodeCfg* __restrict__ cfg,
+                                                      const NodeCost* __restrict__ cost,
+                                                      const uint32_t* __restrict__ hist,
+                                                      const double* __restrict__ thr_tab,
+                                                      const int32_t* __restrict__ thr_row,
+                                                      DpScalars S, double* __restrict__ val,
+                                                      double* __restrict__ mig,
+                                                      int32_t* __restrict__ parent,
+                                                      double* __restrict__ stc,
+                                                      double* __restrict__ stm) {
+  const LevelDesc L = levels[j];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= L.next_count) return;
+  const int ni = L.next_base + warp;
+  const NodeCfg nx = cfg[ni];
+  const NodeCost nc = cost[ni];
+  Cand best{0.0, 0.0, 0.0, 0.0, -1};
+  for (int pi = lane; pi < L.prev_count; pi += 32) {
+    const int gi = L.prev_base + pi;
+    const NodeCfg pv = cfg[gi];
+    const PhiOut ph = phi_dev(pv, nx, nc, L, S, hist, thr_tab, thr_row);
+    const double v = __dadd_rn(val[gi], ph.committed);
+    const double mg = __dadd_rn(mig[gi], ph.mig);
+    if (best.idx < 0 || v > best.value || (v == best.value && mg < best.mig)) {
+      best.value = v;
+      best.mig = mg;
+      best.stc = ph.committed;
+      best.stm = ph.mig;
+      best.idx = pi;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const Cand o = shfl_cand(best, lane ^ off);
+    if (cand_better(o, best)) best = o;
+  }
+  if (lane == 0) {
+    val[ni] = best.value;
+    mig[ni] = best.mig;
+    parent[ni] = best.idx;
+    stc[ni] = best.stc;
+    stm[ni] = best.stm;
+  }
+}
+
+// Final pick (rank = (value, -mig, D, -P), suspended = (-1, 0), first index
+// wins) and traceback into PlanStep[horizon].  One block of 256 threads.
+__global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restrict__ levels,
+                                                       int horizon,
+                                                       const NodeCfg* __restrict__ cfg,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ mig,
+                                                       const int32_t* __restrict__ parent,
+                                                       const double* __restrict__ stc,
+                                                       const double* __restrict__ stm,
+                                                       lp_plan_step* __restrict__ plan,
+                                                       double* __restrict__ final_value) {
+  __shared__ int s_idx[256];
+  const LevelDesc last = levels[horizon - 1];
+  const int base = last.next_base, cnt = last.next_count;
+  auto gt = [&](int a, int b) -> bool {  // rank(a) > rank(b)
+    if (b < 0) return a >= 0;
+    if (a < 0) return false;
+    const double va = val[base + a], vb = val[base + b];
+    if (vb < va) return true;
+    if (va < vb) return false;
+    const double ma = -mig[base + a], mb = -mig[base + b];
+    if (mb < ma) return true;
+    if (ma < mb) return false;
+    const NodeCfg ca = cfg[base + a], cb = cfg[base + b];
+    const int da = ca.d > 0 ? ca.d : -1, db = cb.d > 0 ? cb.d : -1;
+    if (db < da) return true;
+    if (da < db) return false;
+    const int pa = ca.d > 0 ? -ca.p : 0, pb = cb.d > 0 ? -cb.p : 0;
+    return pb < pa;
+  };
+  int mine = -1;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    if (gt(i, mine)) mine = i;  // ascending i: strict > keeps the first
+  s_idx[threadIdx.x] = mine;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const int a = s_idx[threadIdx.x], b = s_idx[threadIdx.x + s];
+      // ties between different threads' winners: lower index wins
+      if (gt(b, a) || (b >= 0 && a >= 0 && !gt(a, b) && b < a)) s_idx[threadIdx.x] = b;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int idx = s_idx[0];
+    if (final_value) *final_value = val[base + idx];
+    for (int jj = horizon; jj >= 1; --jj) {
+      const LevelDesc Lj = levels[jj - 1];
+      const int gi = Lj.next_base + idx;
+      const NodeCfg c = cfg[gi];
+      lp_plan_step st;
+      st.interval_index = jj;
+      st.config.pipelines = c.d > 0 ? c.d : 0;
+      st.config.stages = c.d > 0 ? c.p : 0;
+      st.expected_committed = stc[gi];
+      st.expected_mig_cost_s = stm[gi];
+      plan[jj - 1] = st;
+      idx = parent[gi];
+    }
+  }
+}
+
+// Liveput table: for each (level with histogram, prev config) row,
+// sum_m count_m * throughput(m, P) / count (expected_liveput semantics,
+// preemption.cpp:87-112, intra-stage recovery).
+__global__ void liveput_kernel(const int4* __restrict__ rows /* level, node, out_row, - */,
+                               int n_rows, const LevelDesc* __restrict__ levels,
+                               const NodeCfg* __restrict__ cfg, const uint32_t* __restrict__ hist,
+                               const double* __restrict__ thr_tab,
+                               const int32_t* __restrict__ thr_row,
+                               lp_liveput_row* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  const int4 rw = rows[r];
+  const LevelDesc L = levels[rw.x];
+  const NodeCfg c = cfg[rw.y];
+  const uint32_t* h = hist + c.hist_off;
+  const int dmax = min(L.k, c.d);
+  double acc = 0.0;
+  for (int d = dmax; d >= 0; --d) {
+    const int m = c.d - d;
+    if (m < 1 || h[d] == 0u) continue;
+    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(h[d]), thr_tab[thr_row[c.p] + m]));
+  }
+  lp_liveput_row o;
+  o.interval = rw.x;
+  o.config.pipelines = c.d;
+  o.config.stages = c.p;
+  o.liveput = __ddiv_rn(acc, static_cast<double>(L.total));
+  out[rw.z] = o;
+}
+
+// Single phi evaluation (lp_phi): one thread.
+__global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc L, DpScalars S,
+                                  const uint32_t* __restrict__ hist,
+                                  const double* __restrict__ thr_tab,
+                                  const int32_t* __restrict__ thr_row, double* __restrict__ out2) {
+  const PhiOut o = phi_dev(pv, nx, nc, L, S, hist, thr_tab, thr_row);
+  out2[0] = o.committed;
+  out2[1] = o.mig;
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
+                           const NodeCfg* cfg, const NodeCost* cost, const uint32_t* hist,
+                           const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
+                           double* val, double* mig, int32_t* parent, double* stc, double* stm) {
+  const int threads = 256;
+  const int warps_per_block = threads / 32;
+  const int blocks = (next_count + warps_per_block - 1) / warps_per_block;
+  if (blocks <= 0) return cudaSuccess;
+  dp_step_kernel<<<blocks, threads, 0, st>>>(j, levels, cfg, cost, hist, thr_tab, thr_row, S, val,
+                                             mig, parent, stc, stm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
+                            const NodeCfg* cfg, const double* val, const double* mig,
+                            const int32_t* parent, const double* stc, const double* stm,
+                            lp_plan_step* plan, double* final_value) {
+  dp_final_kernel<<<1, 256, 0, st>>>(levels, horizon, cfg, val, mig, parent, stc, stm, plan,
+                                     final_value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_liveput(int n_rows, cudaStream_t st, const int4* rows, const LevelDesc* levels,
+                           const NodeCfg* cfg, const uint32_t* hist, const double* thr_tab,
+                           const int32_t* thr_row, lp_liveput_row* out) {
+  if (n_rows <= 0) return cudaSuccess;
+  liveput_kernel<<<(n_rows + 127) / 128, 128, 0, st>>>(rows, n_rows, levels, cfg, hist, thr_tab,
+                                                       thr_row, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
+                              const LevelDesc& L, const DpScalars& S, const uint32_t* hist,
+                              const double* thr_tab, const int32_t* thr_row, double* out2,
+                              cudaStream_t st) {
+  phi_single_kernel<<<1, 1, 0, st>>>(pv, nx, nc, L, S, hist, thr_tab, thr_row, out2);
+  return cudaGetLastError();
+}
+
+}  // namespace lp

@@ -1,0 +1,42 @@
+// lp_launch.h — host-callable launch wrappers of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "liveput.h"
+#include "lp_layout.h"
+
+namespace lp {
+
+cudaError_t launch_hist_regs(int kmax, bool smem_evt, int blocks, size_t smem, cudaStream_t st,
+                             const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
+                             const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
+                             uint32_t* h0);
+cudaError_t launch_hist_ctr(bool smem_evt, int blocks, int threads, size_t smem, int pmax_cap,
+                            cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
+                            const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
+                            uint32_t* evt, uint32_t* h0);
+cudaError_t launch_finalize(int n_pairs, int n_entries, cudaStream_t st, const PairDesc* pairs,
+                            const EntryDesc* ents, uint32_t* evt, uint32_t* h0, uint32_t* hist);
+cudaError_t launch_dump(int n, int k, int exact, int trials, uint64_t seed, const DrawConst* dc,
+                        const uint64_t* binom, int binom_stride, uint32_t* gscratch,
+                        uint16_t* sorted_out, const int2* cfgs, int n_cfg, uint16_t* m_out,
+                        cudaStream_t st);
+
+cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
+                           const NodeCfg* cfg, const NodeCost* cost, const uint32_t* hist,
+                           const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
+                           double* val, double* mig, int32_t* parent, double* stc, double* stm);
+cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
+                            const NodeCfg* cfg, const double* val, const double* mig,
+                            const int32_t* parent, const double* stc, const double* stm,
+                            lp_plan_step* plan, double* final_value);
+cudaError_t launch_liveput(int n_rows, cudaStream_t st, const int4* rows, const LevelDesc* levels,
+                           const NodeCfg* cfg, const uint32_t* hist, const double* thr_tab,
+                           const int32_t* thr_row, lp_liveput_row* out);
+cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
+                              const LevelDesc& L, const DpScalars& S, const uint32_t* hist,
+                              const double* thr_tab, const int32_t* thr_row, double* out2,
+                              cudaStream_t st);
+
+}  // namespace lp

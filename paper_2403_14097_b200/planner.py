@@ -1,0 +1,209 @@
+"""Python mirror of ``spotsim::Planner`` (optimizer.hpp:41-92) over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference: ``None``
+is the suspended configuration (std::nullopt), bad arguments raise
+ValueError (the reference's std::invalid_argument).  Every computation runs
+in libliveput.so on the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+from .model import (CostTable, ParallelConfig, PlannerOptions, PlanStep, WorkloadProfile,
+                    cfg_from_c, cfg_to_c)
+
+
+@dataclass
+class PhiValue:
+    committed: float = 0.0
+    mig_cost_s: float = 0.0
+
+
+@dataclass
+class LiveputRow:
+    interval: int
+    config: ParallelConfig
+    liveput: float
+
+
+class Planner:
+    """Availability-aware configuration planner (liveput DP) on one B200."""
+
+    def __init__(self, w: WorkloadProfile, costs: Optional[CostTable] = None,
+                 opt: Optional[PlannerOptions] = None, device: int = 0):
+        self._lib = _abi.lib()
+        self.w = w
+        self.costs = costs or CostTable()
+        self.opt = opt or PlannerOptions()
+        self._prof, self._keep = w.to_c()
+        self._c = self.costs.to_c()
+        self._o = self.opt.to_c()
+        h = C.c_void_p()
+        _abi.check(self._lib.lp_create(C.byref(self._prof), C.byref(self._c), C.byref(self._o),
+                                       device, C.byref(h)))
+        self._h = h
+        self.last_liveput: List[LiveputRow] = []
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- reference API -------------------------------------------------
+    def workload(self) -> WorkloadProfile:
+        return self.w
+
+    def options(self) -> PlannerOptions:
+        return self.opt
+
+    def phi(self, prev: Optional[ParallelConfig], nxt: Optional[ParallelConfig], n_now: int,
+            n_next: int) -> PhiValue:
+        c, m = C.c_double(), C.c_double()
+        _abi.check(self._lib.lp_phi(self._h, cfg_to_c(prev), cfg_to_c(nxt), n_now, n_next,
+                                    C.byref(c), C.byref(m)), self._h)
+        return PhiValue(c.value, m.value)
+
+    def dp_optimize(self, current: Optional[ParallelConfig], n_seq: Sequence[int],
+                    want_liveput: bool = False) -> List[PlanStep]:
+        n = len(n_seq)
+        if n < 2:
+            raise ValueError("dp_optimize: need at least N_i and N_{i+1}")
+        ns = (C.c_int32 * n)(*n_seq)
+        out = (_abi.lp_plan_step * (n - 1))()
+        cap = 0
+        live = None
+        rows = C.c_int32(0)
+        if want_liveput:
+            cap = sum(len(self.configs(x)) for x in n_seq) + 1
+            live = (_abi.lp_liveput_row * cap)()
+        _abi.check(self._lib.lp_replan(self._h, cfg_to_c(current), ns, n, out, live, cap,
+                                       C.byref(rows)), self._h)
+        if want_liveput:
+            self.last_liveput = [LiveputRow(r.interval, cfg_from_c(r.config), r.liveput)
+                                 for r in live[: min(rows.value, cap)]]
+        return [PlanStep(s.interval_index, cfg_from_c(s.config), s.expected_committed,
+                         s.expected_mig_cost_s) for s in out]
+
+    def sequence_value(self, current: Optional[ParallelConfig],
+                       sequence: Sequence[Optional[ParallelConfig]], n_seq: Sequence[int]) -> float:
+        if len(sequence) + 1 != len(n_seq):
+            raise ValueError("sequence_value: sequence/N length mismatch")
+        seq = (_abi.lp_config * max(len(sequence), 1))(*[cfg_to_c(c) for c in sequence])
+        ns = (C.c_int32 * len(n_seq))(*n_seq)
+        out = C.c_double()
+        _abi.check(self._lib.lp_sequence_value(self._h, cfg_to_c(current), seq, ns, len(n_seq),
+                                               C.byref(out)), self._h)
+        return out.value
+
+    # ---- hot-path internals exposed for parity -------------------------
+    def survivor_counts(self, prev: ParallelConfig, n_now: int, n_minus: int) -> Tuple[np.ndarray, int]:
+        counts = (C.c_uint64 * (prev.pipelines + 1))()
+        tot = C.c_uint64()
+        _abi.check(self._lib.lp_survivor_hist(self._h, prev.to_c(), n_now, n_minus, counts,
+                                              C.byref(tot)), self._h)
+        return np.array(counts[:], dtype=np.uint64), tot.value
+
+    def survivor_histogram(self, prev: ParallelConfig, n_now: int, n_minus: int) -> np.ndarray:
+        counts, tot = self.survivor_counts(prev, n_now, n_minus)
+        return counts.astype(np.float64) / float(tot)
+
+    def expected_liveput(self, cfg: ParallelConfig, n: int, n_minus: int, exact: bool = True,
+                         trials: int = 1000, seed: int = 0) -> float:
+        out = C.c_double()
+        _abi.check(self._lib.lp_expected_liveput(self._h, cfg.to_c(), n, n_minus, int(exact), trials,
+                                                 seed, C.byref(out)), self._h)
+        return out.value
+
+    def dump_survivors(self, n: int, n_minus: int, trials: int, seed: int,
+                       cfgs: Sequence[ParallelConfig], exact: bool = False) -> np.ndarray:
+        arr = (_abi.lp_config * len(cfgs))(*[c.to_c() for c in cfgs])
+        out = np.zeros((trials, len(cfgs)), dtype=np.uint16)
+        _abi.check(self._lib.lp_dump_survivors(
+            self._h, n, n_minus, int(exact), trials, seed, arr, len(cfgs),
+            out.ctypes.data_as(C.POINTER(C.c_uint16))), self._h)
+        return out
+
+    def dump_scenarios(self, n: int, n_minus: int, trials: int, seed: int) -> np.ndarray:
+        out = np.zeros((trials, max(n_minus, 1)), dtype=np.uint16)
+        _abi.check(self._lib.lp_dump_scenarios(self._h, n, n_minus, trials, seed,
+                                               out.ctypes.data_as(C.POINTER(C.c_uint16))), self._h)
+        return out[:, :n_minus]
+
+    # ---- split re-plan for device-resident timing ----------------------
+    def prepare(self, current: Optional[ParallelConfig], n_seq: Sequence[int]) -> None:
+        ns = (C.c_int32 * len(n_seq))(*n_seq)
+        _abi.check(self._lib.lp_prepare(self._h, cfg_to_c(current), ns, len(n_seq)), self._h)
+
+    def execute(self) -> None:
+        _abi.check(self._lib.lp_execute(self._h), self._h)
+
+    def fetch(self, horizon: int) -> List[PlanStep]:
+        out = (_abi.lp_plan_step * horizon)()
+        _abi.check(self._lib.lp_fetch(self._h, out, None, 0, None), self._h)
+        return [PlanStep(s.interval_index, cfg_from_c(s.config), s.expected_committed,
+                         s.expected_mig_cost_s) for s in out]
+
+    def stats(self) -> _abi.lp_stats:
+        st = _abi.lp_stats()
+        _abi.check(self._lib.lp_get_stats(self._h, C.byref(st)), self._h)
+        return st
+
+    def stream_ptr(self) -> int:
+        return self._lib.lp_stream(self._h) or 0
+
+    def comm_init(self, uid: bytes, nranks: int, rank: int) -> None:
+        arr = (C.c_uint8 * _abi.LP_NCCL_ID_BYTES).from_buffer_copy(uid)
+        _abi.check(self._lib.lp_comm_init(self._h, arr, nranks, rank), self._h)
+
+    # ---- host table producers -----------------------------------------
+    def configs(self, n: int) -> List[ParallelConfig]:
+        return enumerate_configs(n, self.w)
+
+
+def nccl_unique_id() -> bytes:
+    arr = (C.c_uint8 * _abi.LP_NCCL_ID_BYTES)()
+    _abi.check(_abi.lib().lp_nccl_unique_id(arr))
+    return bytes(arr)
+
+
+def enumerate_configs(n: int, w: WorkloadProfile) -> List[ParallelConfig]:
+    """perf_model.cpp:44-52 (host table producer)."""
+    lib = _abi.lib()
+    p, keep = w.to_c()
+    cnt = lib.lp_enumerate_configs(C.byref(p), n, None, 0)
+    out = (_abi.lp_config * max(cnt, 1))()
+    lib.lp_enumerate_configs(C.byref(p), n, out, cnt)
+    return [ParallelConfig(out[i].pipelines, out[i].stages) for i in range(cnt)]
+
+
+def throughput(cfg: ParallelConfig, w: WorkloadProfile) -> float:
+    p, keep = w.to_c()
+    return _abi.lib().lp_throughput(C.byref(p), cfg.to_c())
+
+
+def reactive_plan(n_now: int, w: WorkloadProfile) -> Optional[ParallelConfig]:
+    p, keep = w.to_c()
+    out = _abi.lp_config()
+    return cfg_from_c(out) if _abi.lib().lp_reactive_plan(C.byref(p), n_now, C.byref(out)) else None
+
+
+def scenario_count(n: int, k: int) -> int:
+    return _abi.lib().lp_scenario_count(n, k)
+
+
+def mix_seed(a: int, b: int) -> int:
+    return _abi.lib().lp_mix_seed(a, b)

@@ -1,0 +1,264 @@
+"""GPU parity: libliveput.so (sm_100a) against the reference's golden vectors and
+the CPU oracle, through the C ABI.  Integer results (scenarios, survivor
+minima, histogram counts) and the strategy sequence must match bit-exactly;
+FP64 phi / plan values are bit-exact too (tolerance 0) because every device
+FP64 op is an explicit round-to-nearest intrinsic in the reference's order.
+expected_liveput sums in a different order: tolerance 1e-12 relative."""
+import numpy as np
+import pytest
+
+from conftest import load_golden, profile_by_name, profile_from_dict, unhex
+from oracle import oracle as O
+from paper_2403_14097_b200.model import (CostTable, ParallelConfig, PlannerOptions, lm_1p5b, lm_6p7b,
+                                         resnet152_dp, toy_six_instance)
+
+pytestmark = pytest.mark.gpu
+
+KNOWN_NSEQ = [32, 28, 28, 26, 29, 26, 26, 21, 23, 23, 21, 25, 22]
+
+
+def cfg(x):
+    return None if x is None else ParallelConfig(*x)
+
+
+def planner(w, opt=None, costs=None):
+    from paper_2403_14097_b200.planner import Planner
+    return Planner(w, costs or CostTable(), opt or PlannerOptions())
+
+
+def plan_rows(plan):
+    return [[s.interval_index, None if s.config is None else [s.config.pipelines, s.config.stages],
+             float.hex(s.expected_committed), float.hex(s.expected_mig_cost_s)] for s in plan]
+
+
+@pytest.fixture(scope="module")
+def gpt2():
+    p = planner(lm_1p5b(), PlannerOptions(mc_trials=10000))
+    yield p
+    p.close()
+
+
+def test_native_library_is_in_tree():
+    from paper_2403_14097_b200 import _abi
+    lib = _abi.lib()
+    assert str(_abi.LIB_PATH).endswith("paper_2403_14097_b200/lib/libliveput.so")
+    assert "sm_100a" in lib.lp_build_info().decode()
+
+
+# ---- scenario generation ---------------------------------------------------
+def test_scenarios_match_reference_sample_vectors(gpt2):
+    for c in load_golden("scenarios")["sample_vectors"]:
+        got = gpt2.dump_scenarios(c["n"], c["k"], c["trials"], c["seed"])
+        assert got.astype(int).tolist() == c["sets"], (c["n"], c["k"])
+
+
+def test_known_answer_trials(gpt2):
+    seed = O.planner_seed(0x5EED, 32, 3)
+    got = gpt2.dump_scenarios(32, 3, 4, seed)
+    assert got.tolist() == [[6, 8, 25], [18, 29, 31], [0, 6, 16], [5, 18, 29]]
+
+
+def test_survivor_minima_match_reference(gpt2):
+    for c in load_golden("survivors"):
+        cfgs = [ParallelConfig(*x) for x in c["configs"]]
+        got = gpt2.dump_survivors(c["n"], c["k"], c["trials"], c["seed"], cfgs)
+        assert got.astype(int).tolist() == c["m"], (c["profile"], c["n"], c["k"])
+
+
+def test_exact_enumeration_order(gpt2):
+    for c in load_golden("scenarios")["enumerate_vectors"]:
+        if c["k"] == 0:
+            continue
+        cnt = len(c["sets"])
+        cfgs = [ParallelConfig(1, 1)]
+        got = gpt2.dump_survivors(c["n"], c["k"], cnt, 0, cfgs, exact=True)
+        # survivors of config (1,1): 0 iff slot 0 preempted
+        assert got[:, 0].tolist() == [0 if s[0] == 0 else 1 for s in c["sets"]]
+
+
+# ---- histograms ----------------------------------------------------------------
+def test_histograms_match_reference():
+    by = {}
+    for c in load_golden("histograms"):
+        by.setdefault((c["profile"], c["mc_trials"]), []).append(c)
+    for (prof, trials), cases in by.items():
+        p = planner(profile_by_name(prof), PlannerOptions(mc_trials=trials))
+        for c in cases:
+            h = p.survivor_histogram(ParallelConfig(*c["cfg"]), c["n"], c["k"])
+            assert [float.hex(x) for x in h] == c["hist"], c
+        p.close()
+
+
+def test_known_answer_histogram(gpt2):
+    counts, tot = gpt2.survivor_counts(ParallelConfig(4, 7), 32, 3)
+    assert counts.tolist() == [0, 46, 2412, 7535, 7] and tot == 10000
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_ensembles_vs_oracle(seed):
+    """Both kernel variants (k <= 16 registers, k > 16 counters), random n/k,
+    every config of n, bit-exact counts."""
+    rng = np.random.default_rng(1000 + seed)
+    for prof in ("lm_1p5b", "resnet152", "lm_6p7b"):
+        w = profile_by_name(prof)
+        n = int(rng.integers(20, 520))
+        k = int(rng.choice([1, 2, 3, 5, 8, 11, 16, 17, 24, 40, 63, min(n - 1, 100)]))
+        k = min(k, n)
+        trials = int(rng.integers(500, 5000))
+        opt = PlannerOptions(mc_trials=trials, exact_cap=0)
+        p = planner(w, opt)
+        cs = O.oracle_configs(w, n)
+        if not cs:
+            p.close()
+            continue
+        sel = [cs[i] for i in sorted(set(rng.integers(0, len(cs), 12).tolist()))]
+        ref, tot = O.oracle_ensemble_counts(n, k, False, trials, O.planner_seed(0x5EED, n, k), sel)
+        for ci, c in enumerate(sel):
+            got, gt = p.survivor_counts(c, n, k)
+            assert gt == tot
+            assert got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (prof, n, k, c)
+        p.close()
+
+
+def test_exact_branch_counts_vs_oracle():
+    w = lm_1p5b()
+    p = planner(w, PlannerOptions(exact_cap=1000000))
+    for n, k in [(64, 2), (40, 3), (20, 10), (21, 18), (30, 29), (12, 0), (9, 9), (100, 1)]:
+        cs = O.oracle_configs(w, n)
+        if not cs:
+            continue
+        ref, tot = O.oracle_ensemble_counts(n, k, True, 0, 0, cs)
+        for ci, c in enumerate(cs):
+            got, gt = p.survivor_counts(c, n, k)
+            assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, c)
+    p.close()
+
+
+# ---- phi, plans ---------------------------------------------------------------
+def test_phi_matches_reference():
+    for c in load_golden("phi"):
+        p = planner(profile_by_name(c["profile"]),
+                    PlannerOptions(mc_trials=c["mc_trials"], strict_conditional=c["strict"]))
+        v = p.phi(cfg(c["prev"]), cfg(c["next"]), c["n_now"], c["n_next"])
+        assert (v.committed, v.mig_cost_s) == (unhex(c["committed"]), unhex(c["mig"])), c
+        p.close()
+
+
+def test_known_answer_plan(gpt2):
+    plan = gpt2.dp_optimize(ParallelConfig(4, 8), KNOWN_NSEQ)
+    assert [s.config for s in plan] == [ParallelConfig(3, 8)] * 6 + [ParallelConfig(3, 7)] * 6
+    v = gpt2.sequence_value(ParallelConfig(4, 8), [s.config for s in plan], KNOWN_NSEQ)
+    assert v == 8460.1874990222786
+
+
+def test_plans_match_reference():
+    for c in load_golden("plans"):
+        p = planner(profile_by_name(c["profile"]),
+                    PlannerOptions(mc_trials=c["mc_trials"], exact_cap=c["exact_cap"],
+                                   strict_conditional=c["strict"]))
+        plan = p.dp_optimize(cfg(c["current"]), c["n_seq"])
+        assert plan_rows(plan) == c["plan"], c["tag"]
+        assert float.hex(p.sequence_value(cfg(c["current"]), [s.config for s in plan], c["n_seq"])) == c["value"]
+        p.close()
+
+
+def test_random_small_dp_match_reference():
+    for c in load_golden("random_dp"):
+        p = planner(profile_from_dict(c["profile"]), PlannerOptions(**c["options"]), CostTable(**c["costs"]))
+        assert plan_rows(p.dp_optimize(cfg(c["current"]), c["n_seq"])) == c["plan"]
+        p.close()
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_large_replans_vs_oracle(case):
+    """N=256..512 re-plans (MC branch, both kernel variants, multi-work-item
+    splits) against the cache-free oracle; beyond N=256 the reference's phi
+    cache aliases, so the oracle is the checker there."""
+    w = [lm_1p5b(), lm_1p5b(), resnet152_dp(), lm_6p7b()][case]
+    n_seq = [[256, 224, 224, 208, 232, 208, 208, 168, 184],
+             [512, 480, 488, 470, 470, 500, 430],
+             [64, 40, 52, 30, 61, 44, 44, 20],
+             [128, 120, 121, 110, 118, 104, 104, 96, 100]][case]
+    trials = [2000, 500, 3000, 4000][case]
+    opt = PlannerOptions(mc_trials=trials)
+    cur = O.oracle_reactive(w, n_seq[0])
+    ref = O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, n_seq)
+    p = planner(w, opt)
+    got = p.dp_optimize(cur, n_seq)
+    assert plan_rows(got) == plan_rows(ref)
+    p.close()
+
+
+def test_liveput_table_and_expected_liveput():
+    g = load_golden("tables")["liveput"]
+    for c in g:
+        p = planner(profile_by_name(c["profile"]))
+        v = p.expected_liveput(ParallelConfig(*c["cfg"]), c["n"], c["k"], bool(c["exact"]), c["trials"], c["seed"])
+        assert v == pytest.approx(unhex(c["value"]), rel=1e-12, abs=1e-12), c
+        p.close()
+    w = lm_1p5b()
+    opt = PlannerOptions(mc_trials=3000)
+    p = planner(w, opt)
+    op = O.OraclePlanner(w, CostTable(), opt)
+    ns = [64, 60, 60, 57]
+    p.dp_optimize(ParallelConfig(8, 8), ns, want_liveput=True)
+    rows = p.last_liveput
+    assert len(rows) == 1 + len(O.oracle_configs(w, 60)) * 2
+    for r in rows[:40]:
+        k = max(0, ns[r.interval] - ns[r.interval + 1])
+        assert r.liveput == pytest.approx(op.liveput(r.config, ns[r.interval], k), rel=1e-12)
+    p.close()
+
+
+# ---- edge cases and errors ---------------------------------------------------
+def test_edge_cases_vs_oracle():
+    w = toy_six_instance()
+    for opt in (PlannerOptions(exact_cap=0, mc_trials=50), PlannerOptions(exact_cap=100000),
+                PlannerOptions(mc_trials=1, exact_cap=1)):
+        p = planner(w, opt)
+        op = O.OraclePlanner(w, CostTable(), opt)
+        for cur, ns in [(ParallelConfig(2, 3), [6, 6, 0, 6]), (ParallelConfig(2, 3), [6, 0, 0]),
+                        (None, [0, 0, 6]), (ParallelConfig(3, 2), [6, 6]), (ParallelConfig(1, 2), [6, 1, 2, 6, 6, 5])]:
+            assert plan_rows(p.dp_optimize(cur, ns)) == plan_rows(op.dp_optimize(cur, ns)), (opt, cur, ns)
+        p.close()
+
+
+def test_errors():
+    from paper_2403_14097_b200._abi import LiveputError
+    p = planner(lm_1p5b())
+    with pytest.raises(ValueError):
+        p.dp_optimize(None, [32])
+    with pytest.raises(ValueError):
+        p.dp_optimize(ParallelConfig(4, 8), [16, 16])  # current exceeds n_seq[0]
+    with pytest.raises(ValueError):
+        p.sequence_value(None, [None], [8, 8, 8])
+    with pytest.raises(LiveputError):
+        p.dp_optimize(None, [4096, 4000])
+    p.close()
+    p = planner(lm_1p5b(), PlannerOptions(mc_trials=0))
+    with pytest.raises(ValueError):
+        p.dp_optimize(ParallelConfig(4, 8), [32, 28])  # sample_vectors: trials must be >= 1
+    p.close()
+    p = planner(lm_1p5b(), PlannerOptions(exact_cap=10**12))
+    with pytest.raises(ValueError):
+        p.dp_optimize(ParallelConfig(4, 8), [64, 48])  # enumerate_vectors: too large
+    p.close()
+
+
+def test_full_size_properties():
+    """BASELINE config 4 shape (N=256, I=24, 1e6 samples): integer histograms
+    sum to the trial count and the plan is deterministic across runs."""
+    from bench import north_star_nseq
+    w = lm_1p5b()
+    p = planner(w, PlannerOptions(mc_trials=1000000))
+    ns = north_star_nseq(256, 24)
+    cur = O.oracle_reactive(w, ns[0])
+    a = p.dp_optimize(cur, ns)
+    st = p.stats()
+    assert st.resolutions > 5e9
+    b = p.dp_optimize(cur, ns)
+    assert plan_rows(a) == plan_rows(b)
+    for c in [ParallelConfig(36, 7), ParallelConfig(3, 80), ParallelConfig(1, 224)]:
+        counts, tot = p.survivor_counts(c, 224, 16)
+        assert int(counts.sum()) == tot == 1000000
+    p.close()
