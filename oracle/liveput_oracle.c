@@ -291,6 +291,14 @@ static void* ens_worker(void* arg) {
   int* cnt = (int*)calloc((size_t)(n > 0 ? n : 1), sizeof(int));
   int* idx = (int*)malloc(sizeof(int) * (k > 0 ? k : 1));
   for (int i = 0; i < k; ++i) idx[i] = i;
+  if (jb->exact && k > 0)
+    for (long long t = 0; t < jb->t0; ++t) { /* walk to the first rank of the range */
+      int i = k - 1;
+      while (i >= 0 && idx[i] == n - k + i) --i;
+      if (i < 0) break;
+      ++idx[i];
+      for (int j = i + 1; j < k; ++j) idx[j] = idx[j - 1] + 1;
+    }
   for (long long t = jb->t0; t < jb->t1; ++t) {
     if (jb->exact) {
       for (int i = 0; i < k; ++i) s[i] = idx[i];
@@ -317,8 +325,27 @@ static void* ens_worker(void* arg) {
   return NULL;
 }
 
+static int ensemble_range(int n, int k, int exact, int trials, uint64_t seed, const int* cfg,
+                          int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads,
+                          long long r0, long long r1);
+
 int or_ensemble_counts(int n, int k, int exact, int trials, uint64_t seed, const int* cfg,
                        int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads) {
+  return ensemble_range(n, k, exact, trials, seed, cfg, n_cfg, counts, stride, total, threads, 0,
+                        -1);
+}
+
+/* Partial ensemble over scenario ranks [r0, r1) — the multi-rank split. */
+int or_ensemble_counts_range(int n, int k, int exact, int trials, uint64_t seed, const int* cfg,
+                             int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads,
+                             long long r0, long long r1) {
+  return ensemble_range(n, k, exact, trials, seed, cfg, n_cfg, counts, stride, total, threads, r0,
+                        r1);
+}
+
+static int ensemble_range(int n, int k, int exact, int trials, uint64_t seed, const int* cfg,
+                          int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads,
+                          long long r0, long long r1) {
   if (k < 0 || k > n) {
     set_err("bad n_minus");
     return -1;
@@ -343,14 +370,17 @@ int or_ensemble_counts(int n, int k, int exact, int trials, uint64_t seed, const
   }
   if (threads < 1) threads = 1;
   if (threads > 64) threads = 64;
+  if (r1 < 0 || r1 > T) r1 = T;
+  if (r0 < 0) r0 = 0;
+  if (r0 > r1) r0 = r1;
   memset(counts, 0, sizeof(uint64_t) * (size_t)n_cfg * stride);
   pthread_t th[64];
   ens_job jobs[64];
   uint64_t* part[64];
   for (int i = 0; i < threads; ++i) {
     part[i] = (uint64_t*)calloc((size_t)n_cfg * stride, sizeof(uint64_t));
-    jobs[i] = (ens_job){n, k, exact, T * i / threads, T * (i + 1) / threads, seed,
-                        cfg, n_cfg, stride, part[i]};
+    jobs[i] = (ens_job){n, k, exact, r0 + (r1 - r0) * i / threads, r0 + (r1 - r0) * (i + 1) / threads,
+                        seed, cfg, n_cfg, stride, part[i]};
     if (threads == 1)
       ens_worker(&jobs[i]);
     else
@@ -361,7 +391,7 @@ int or_ensemble_counts(int n, int k, int exact, int trials, uint64_t seed, const
     for (size_t e = 0; e < (size_t)n_cfg * stride; ++e) counts[e] += part[i][e];
     free(part[i]);
   }
-  *total = (uint64_t)T;
+  *total = (uint64_t)(r1 - r0);
   return 0;
 }
 

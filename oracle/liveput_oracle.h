@@ -61,6 +61,10 @@ int or_scenarios(int n, int k, int exact, int trials, uint64_t seed, int* out_so
 int or_ensemble_counts(int n, int k, int exact, int trials, uint64_t seed, const int* cfg_dp,
                        int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads);
 
+int or_ensemble_counts_range(int n, int k, int exact, int trials, uint64_t seed, const int* cfg_dp,
+                             int n_cfg, uint64_t* counts, int stride, uint64_t* total, int threads,
+                             long long r0, long long r1);
+
 /* Planner-equivalent entry points (PlannerOptions semantics, exact_cap
  * switch and seed derivation of optimizer.cpp:64-94). */
 typedef struct or_planner or_planner;

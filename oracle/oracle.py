@@ -61,6 +61,9 @@ def oracle_lib():
             "or_scenarios": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _P(C.c_int)]),
             "or_ensemble_counts": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _P(C.c_int),
                                              C.c_int, _P(C.c_uint64), C.c_int, _P(C.c_uint64), C.c_int]),
+            "or_ensemble_counts_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _P(C.c_int),
+                                                   C.c_int, _P(C.c_uint64), C.c_int, _P(C.c_uint64), C.c_int,
+                                                   C.c_longlong, C.c_longlong]),
             "or_planner_new": (C.c_void_p, [prof, costs, opts, C.c_int]),
             "or_planner_free": (None, [C.c_void_p]),
             "or_last_error": (C.c_char_p, []),
@@ -267,6 +270,22 @@ def oracle_ensemble_counts(n, k, exact, trials, seed, cfgs: Sequence[ParallelCon
     threads = threads or min(8, os.cpu_count() or 1)
     if L.or_ensemble_counts(n, k, int(exact), trials, seed, _ints(flat), len(cfgs), out, stride,
                             C.byref(tot), threads) != 0:
+        raise ValueError(L.or_last_error().decode())
+    return np.array(out[:], dtype=np.uint64).reshape(len(cfgs), stride), tot.value
+
+
+def oracle_ensemble_counts_range(n, k, exact, trials, seed, cfgs: Sequence[ParallelConfig], r0, r1, threads=0):
+    """Partial ensemble over scenario ranks [r0, r1) (the multi-rank trial split)."""
+    L = oracle_lib()
+    stride = max(c.pipelines for c in cfgs) + 1
+    flat = []
+    for c in cfgs:
+        flat += [c.pipelines, c.stages]
+    out = (C.c_uint64 * (len(cfgs) * stride))()
+    tot = C.c_uint64()
+    threads = threads or min(8, os.cpu_count() or 1)
+    if L.or_ensemble_counts_range(n, k, int(exact), trials, seed, _ints(flat), len(cfgs), out, stride,
+                                  C.byref(tot), threads, r0, r1) != 0:
         raise ValueError(L.or_last_error().decode())
     return np.array(out[:], dtype=np.uint64).reshape(len(cfgs), stride), tot.value
 
