@@ -241,7 +241,7 @@ def test_errors():
     p.close()
     p = planner(lm_1p5b(), PlannerOptions(exact_cap=10**12))
     with pytest.raises(ValueError):
-        p.dp_optimize(ParallelConfig(4, 8), [64, 48])  # enumerate_vectors: too large
+        p.dp_optimize(ParallelConfig(4, 8), [64, 59])  # C(64,5) in (1e6, exact_cap]: enumerate_vectors throws
     p.close()
 
 
@@ -258,7 +258,7 @@ def test_full_size_properties():
     assert st.resolutions > 5e9
     b = p.dp_optimize(cur, ns)
     assert plan_rows(a) == plan_rows(b)
-    for c in [ParallelConfig(36, 7), ParallelConfig(3, 80), ParallelConfig(1, 224)]:
+    for c in [ParallelConfig(32, 7), ParallelConfig(2, 80), ParallelConfig(1, 224)]:
         counts, tot = p.survivor_counts(c, 224, 16)
         assert int(counts.sum()) == tot == 1000000
     p.close()
