@@ -30,6 +30,8 @@ constexpr uint64_t kEnumerationCap = 1000000ULL;  // preemption.hpp:26
 constexpr size_t kSmemBudgetR = 72 * 1024;
 constexpr size_t kSmemBudgetC = 110 * 1024;
 constexpr uint64_t kChunkR = 256 * 8;
+constexpr size_t kScnFixedBudget = 64 * 1024;   // entries + event table per block
+constexpr size_t kSmemBudgetScn = 112 * 1024;   // two blocks per SM
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -137,6 +139,14 @@ size_t smem_ctr(int ne, int k, int n, int64_t evt_len, bool smem_evt, int T, int
          (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(2 * (size_t)k * T) + a16(std::max(gen, ctr));
 }
 
+size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {
+  const size_t nw = (n + 31) / 32;
+  const size_t kk = std::max(k, 1);
+  return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(sizeof(DrawConst) * kk) +
+         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(2 * kk * T) +
+         a16(4 * nw * T) + a16(4 * (size_t)std::max(uw, 1) * T);
+}
+
 // Algorithmic int32-equivalent ops (restated for the
 // threshold-event resolution): S(k) = 20 + 35k per scenario,
 // R(k) = 6k per (scenario, depth); no per-(scenario, config) term.
@@ -230,11 +240,58 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
 
   // work items, grouped by launch configuration
   std::map<std::tuple<int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
+  const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
+  const bool legacy = kenv && std::string(kenv) == "legacy";
   for (int pi = 0; pi < (int)hp.pairs.size(); ++pi) {
     const PairDesc& pd = hp.pairs[pi];
     const uint64_t local = pd.t_hi - pd.t_lo;
     if (local == 0 || pd.n_entries == 0) continue;
     const int e_end = pd.entry_base + pd.n_entries;
+    if (!legacy && pd.k > kMaxKReg) {
+      // scenario-major kernel (lp_hist_scn.cu)
+      const int kreg = (pd.k <= 8) ? 8 : (pd.k <= kMaxKReg ? 16 : 0);
+      int e = pd.entry_base;
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(4 * (size_t)ev2) > kScnFixedBudget)
+            break;
+          ev = ev2;
+          ++e2;
+        }
+        int e_res = e;
+        int pc = 0;
+        while (e_res < e2 && hp.entries[e_res].tmax >= 2) {
+          if (hp.entries[e_res].Dmax > kComb && hp.entries[e_res].P >= 2)
+            pc = std::max(pc, hp.entries[e_res].P);
+          ++e_res;
+        }
+        const int uw = std::max(kreg == 0 ? pd.k : 0, (pc + 1) / 2);
+        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(4 * (size_t)ev) <= kScnFixedBudget;
+        int T = 256;
+        while (T > 32 && smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw) > kSmemBudgetScn) T >>= 1;
+        const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
+        const uint64_t chunk = (uint64_t)T * 16;
+        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.e_res_hi = e_res;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.t0 = t0;
+          w.t1 = std::min(pd.t_hi, t0 + chunk);
+          groups[{2, kreg, T, sm ? 1 : 0}].push_back({w, {smem, uw}});
+        }
+        e = e2;
+      }
+      continue;
+    }
     if (pd.variant == 0) {
       const int km = kmax_for(pd.k);
       int e = pd.entry_base;
@@ -249,6 +306,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           ev = ev2;
           ++e2;
         }
+        int e_res = e;  // depths with Dmax >= 2 (others emit no t >= 2 event)
+        while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
         const bool sm = smem_regs(e2 - e, km, pd.n, ev, true) <= kSmemBudgetR;
         const size_t smem = smem_regs(e2 - e, km, pd.n, ev, sm);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += kChunkR) {
@@ -259,6 +318,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_lo = hp.entries[e].evt_off;
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
+          w.e_res_hi = e_res;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + kChunkR);
           groups[{0, km, 256, sm ? 1 : 0}].push_back({w, {smem, 0}});
@@ -316,6 +376,11 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     for (auto& it : items) {
       hp.work.push_back(it.first);
       size_t s = it.second.first;
+      if (g.kind == 2) {
+        const PairDesc& pd = hp.pairs[it.first.pair];
+        s = smem_scn(it.first.e_res_hi - it.first.e_lo, pd.k, pd.n, it.first.evt_len, g.smem_evt,
+                     g.threads, g.pmax_cap);
+      }
       if (g.kind == 1) {
         const PairDesc& pd = hp.pairs[it.first.pair];
         s = smem_ctr(it.first.e_hi - it.first.e_lo, pd.k, pd.n, it.first.evt_len, g.smem_evt,
@@ -349,7 +414,10 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   if (e != cudaSuccess) return e;
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 0)
+    if (g.kind == 2)
+      e = launch_hist_scn(g.kmax, g.smem_evt, g.count, g.threads, g.smem, g.pmax_cap, st, w, d.pairs,
+                          d.entries, d.draws, d.binom, d.evt, d.h0);
+    else if (g.kind == 0)
       e = launch_hist_regs(g.kmax, g.smem_evt, g.count, g.smem, st, w, d.pairs, d.entries, d.draws,
                            d.binom, d.evt, d.h0);
     else

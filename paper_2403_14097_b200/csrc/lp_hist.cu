@@ -100,12 +100,12 @@ __global__ void __launch_bounds__(256) hist_regs_kernel(const WorkItem* __restri
   extern __shared__ __align__(16) unsigned char smem[];
   const WorkItem w = work[blockIdx.x];
   const PairDesc pd = pairs[w.pair];
-  const int ne = w.e_hi - w.e_lo;
+  const int ne = w.e_res_hi - w.e_lo;  // depths with Dmax >= 2
   const int k = pd.k;
   const bool own_h0 = (w.e_lo == pd.entry_base);
 
   unsigned char* p = smem;
-  EntryDesc* ents = carve<EntryDesc>(p, ne);
+  EntryDesc* ents = carve<EntryDesc>(p, ne > 0 ? ne : 1);
   DrawConst* dc = carve<DrawConst>(p, KMAX);
   uint32_t* h0 = carve<uint32_t>(p, pd.n);
   uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, w.evt_len) : nullptr;

@@ -21,6 +21,7 @@ namespace lp {
 constexpr int kMaxN = 2048;     // instances per availability count (u16 slot ids)
 constexpr int kMaxKReg = 16;    // register-resident scenarios (variant R)
 constexpr int kMaxK = 255;      // u8 class counters (variant C)
+constexpr int kComb = 4;        // scenario-major kernel: Dmax <= kComb uses the bitmap comb
 
 struct PairDesc {
   int32_t n, k;
@@ -63,6 +64,8 @@ struct WorkItem {
   int32_t evt_lo;       // evt offset of e_lo
   int32_t evt_len;      // evt counters of the range (staged in shared memory)
   int32_t smem_evt;     // 1: stage evt in shared memory, 0: global atomics
+  int32_t e_res_hi;     // entries [e_lo, e_res_hi) can emit t >= 2 events (Dmax >= 2)
+  int32_t pad;
   uint64_t t0, t1;      // scenario range
 };
 
