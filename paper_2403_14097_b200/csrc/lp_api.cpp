@@ -32,6 +32,7 @@ constexpr size_t kSmemBudgetC = 110 * 1024;
 constexpr uint64_t kChunkR = 256 * 8;
 constexpr size_t kScnFixedBudget = 64 * 1024;   // entries + event table per block
 constexpr size_t kSmemBudgetScn = 112 * 1024;   // two blocks per SM
+constexpr size_t kSmemBudgetInc = 75 * 1024;    // three blocks per SM
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -118,6 +119,7 @@ struct HistPlan {
   std::vector<DrawConst> draws;
   std::vector<uint64_t> binom;
   std::vector<WorkItem> work;
+  std::vector<uint16_t> divtab;
   std::vector<Group> groups;
   int64_t evt_len = 0, h0_len = 0, hist_len = 0;
   uint64_t scenarios = 0, local_scenarios = 0, resolutions = 0, alg_ops = 0;
@@ -137,6 +139,35 @@ size_t smem_ctr(int ne, int k, int n, int64_t evt_len, bool smem_evt, int T, int
   const size_t ctr = 4 * (size_t)((pmax + 3) / 4) * T;
   return a16(sizeof(EntryDesc) * ne) + a16(sizeof(DrawConst) * k) + a16(4 * (size_t)n) +
          (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(2 * (size_t)k * T) + a16(std::max(gen, ctr));
+}
+
+size_t smem_inc(int ne_res, int kmax, int n, int64_t evt_len, bool smem_evt, int dtab_len, int T) {
+  return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(sizeof(DrawConst) * kmax) +
+         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)evt_len) : 0) +
+         a16(2 * (size_t)std::max(dtab_len, 1)) + a16(4 * (size_t)((ne_res + 1) / 2) * T);
+}
+
+// CSR table: for every difference d in [1, n) the local indices of the
+// resolution depths P >= 2 that divide d (incidence kernel).
+void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n,
+                  std::vector<uint16_t>& out) {
+  std::vector<int> cnt(n + 1, 0);
+  for (int e = e_lo; e < e_res; ++e)
+    if (ents[e].P >= 2)
+      for (int d = ents[e].P; d < n; d += ents[e].P) cnt[d]++;
+  const size_t base = out.size();
+  out.resize(base + n + 1);
+  int acc = 0;
+  for (int d = 0; d <= n; ++d) {
+    out[base + d] = (uint16_t)acc;
+    if (d < n) acc += cnt[d];
+  }
+  out.resize(base + n + 1 + acc);
+  std::vector<int> fill(n + 1, 0);
+  for (int e = e_lo; e < e_res; ++e)
+    if (ents[e].P >= 2)
+      for (int d = ents[e].P; d < n; d += ents[e].P)
+        out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
 }
 
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {
@@ -242,11 +273,56 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   std::map<std::tuple<int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
   const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
   const bool legacy = kenv && std::string(kenv) == "legacy";
+  const bool inc_off = kenv && std::string(kenv) == "noinc";
   for (int pi = 0; pi < (int)hp.pairs.size(); ++pi) {
     const PairDesc& pd = hp.pairs[pi];
     const uint64_t local = pd.t_hi - pd.t_lo;
     if (local == 0 || pd.n_entries == 0) continue;
     const int e_end = pd.entry_base + pd.n_entries;
+    if (!legacy && pd.k <= kMaxKReg && !inc_off) {
+      // sparse incidence kernel (lp_hist_inc.cu)
+      const int km = kmax_for(pd.k);
+      int e = pd.entry_base;
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(4 * (size_t)ev2) > kScnFixedBudget)
+            break;
+          ev = ev2;
+          ++e2;
+        }
+        int e_res = e;
+        while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
+        const int doff = (int)hp.divtab.size();
+        build_divtab(hp.entries, e, e_res, pd.n, hp.divtab);
+        const int dlen = (int)hp.divtab.size() - doff;
+        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(4 * (size_t)ev) <= kScnFixedBudget;
+        int T = 128;
+        while (T > 32 && smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T) > kSmemBudgetInc) T >>= 1;
+        const size_t smem = smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T);
+        const uint64_t chunk = (uint64_t)T * 16;
+        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.e_res_hi = e_res;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.dtab_off = doff;
+          w.dtab_len = dlen;
+          w.t0 = t0;
+          w.t1 = std::min(pd.t_hi, t0 + chunk);
+          groups[{3, km, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
+        }
+        e = e2;
+      }
+      continue;
+    }
     if (!legacy && pd.k > kMaxKReg) {
       // scenario-major kernel (lp_hist_scn.cu)
       const int kreg = (pd.k <= 8) ? 8 : (pd.k <= kMaxKReg ? 16 : 0);
@@ -394,6 +470,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
 }
 
 struct HistDev {
+  const uint16_t* divtab;
   const PairDesc* pairs;
   const EntryDesc* entries;
   const DrawConst* draws;
@@ -414,7 +491,10 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   if (e != cudaSuccess) return e;
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 2)
+    if (g.kind == 3)
+      e = launch_hist_inc(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
+                          d.draws, d.binom, d.divtab, d.evt, d.h0);
+    else if (g.kind == 2)
       e = launch_hist_scn(g.kmax, g.smem_evt, g.count, g.threads, g.smem, g.pmax_cap, st, w, d.pairs,
                           d.entries, d.draws, d.binom, d.evt, d.h0);
     else if (g.kind == 0)
@@ -508,6 +588,7 @@ struct lp_handle {
   std::vector<int4> lrows;
   ThrTable thr;
   DpScalars S{};
+  size_t off_divtab = 0;
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
@@ -553,7 +634,7 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
                       Packer& pk, std::vector<size_t>& extra_offs) {
   (void)extra_offs;
   const size_t op = pk.add(hp.pairs), oe = pk.add(hp.entries), od = pk.add(hp.draws),
-               ob = pk.add(hp.binom), ow = pk.add(hp.work);
+               ob = pk.add(hp.binom), ow = pk.add(hp.work), odt = pk.add(hp.divtab);
   LP_CUDA(h, tables.ensure(pk.bytes.size()));
   LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
   std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
@@ -567,6 +648,7 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
   d.draws = dptr<DrawConst>(tables, od);
   d.binom = dptr<uint64_t>(tables, ob);
   d.work = dptr<WorkItem>(tables, ow);
+  d.divtab = dptr<uint16_t>(tables, odt);
   d.evt = dptr<uint32_t>(work, 0);
   d.h0 = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)));
   d.hist = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)) +
@@ -879,6 +961,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->off_draws = pk.add(h->hp.draws);
   h->off_binom = pk.add(h->hp.binom);
   h->off_work = pk.add(h->hp.work);
+  h->off_divtab = pk.add(h->hp.divtab);
   h->off_levels = pk.add(h->levels);
   h->off_cfg = pk.add(h->cfg);
   h->off_cost = pk.add(h->cost);
@@ -935,6 +1018,7 @@ lp_status lp_execute(lp_handle* h) {
   d.draws = dptr<DrawConst>(h->tables, h->off_draws);
   d.binom = dptr<uint64_t>(h->tables, h->off_binom);
   d.work = dptr<WorkItem>(h->tables, h->off_work);
+  d.divtab = dptr<uint16_t>(h->tables, h->off_divtab);
   d.evt = dptr<uint32_t>(h->work, h->w_evt);
   d.h0 = dptr<uint32_t>(h->work, h->w_h0);
   d.hist = dptr<uint32_t>(h->work, h->w_hist);

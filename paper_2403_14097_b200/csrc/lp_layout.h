@@ -65,6 +65,8 @@ struct WorkItem {
   int32_t evt_len;      // evt counters of the range (staged in shared memory)
   int32_t smem_evt;     // 1: stage evt in shared memory, 0: global atomics
   int32_t e_res_hi;     // entries [e_lo, e_res_hi) can emit t >= 2 events (Dmax >= 2)
+  int32_t dtab_off;     // incidence kernel: divisor table (u16) of this entry range
+  int32_t dtab_len;     //   [n+1 CSR offsets][local depth indices]
   int32_t pad;
   uint64_t t0, t1;      // scenario range
 };
