@@ -33,6 +33,7 @@ constexpr uint64_t kChunkR = 256 * 8;
 constexpr size_t kScnFixedBudget = 64 * 1024;   // entries + event table per block
 constexpr size_t kSmemBudgetScn = 112 * 1024;   // two blocks per SM
 constexpr size_t kSmemBudgetInc = 75 * 1024;    // three blocks per SM
+constexpr int kIncMaxK = 8;                     // incidence kernel up to k = 8, rows above
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -170,6 +171,14 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
         out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
 }
 
+size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int kreg) {
+  const size_t nw = (n + 31) / 32;
+  const size_t kk = std::max(k, 1);
+  return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(sizeof(DrawConst) * kk) +
+         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(4 * (nw + 1) * T) +
+         (kreg == 0 ? a16(4 * kk * T) + a16(2 * kk * T) : 0);
+}
+
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {
   const size_t nw = (n + 31) / 32;
   const size_t kk = std::max(k, 1);
@@ -274,12 +283,52 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
   const bool legacy = kenv && std::string(kenv) == "legacy";
   const bool inc_off = kenv && std::string(kenv) == "noinc";
+  const bool rows_off = kenv && std::string(kenv) == "norows";
   for (int pi = 0; pi < (int)hp.pairs.size(); ++pi) {
     const PairDesc& pd = hp.pairs[pi];
     const uint64_t local = pd.t_hi - pd.t_lo;
     if (local == 0 || pd.n_entries == 0) continue;
     const int e_end = pd.entry_base + pd.n_entries;
-    if (!legacy && pd.k <= kMaxKReg && !inc_off) {
+    if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512) {
+      // bit-sliced row kernel (lp_hist_rows.cu)
+      const int kreg = pd.k <= kMaxKReg ? 16 : 0;
+      int e = pd.entry_base;
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(4 * (size_t)ev2) > kScnFixedBudget)
+            break;
+          ev = ev2;
+          ++e2;
+        }
+        int e_res = e;
+        while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
+        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(4 * (size_t)ev) <= kScnFixedBudget;
+        int T = 256;
+        while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg) > kSmemBudgetScn) T >>= 1;
+        const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg);
+        const uint64_t chunk = (uint64_t)T * 16;
+        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.e_res_hi = e_res;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.t0 = t0;
+          w.t1 = std::min(pd.t_hi, t0 + chunk);
+          groups[{4, kreg, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
+        }
+        e = e2;
+      }
+      continue;
+    }
+    if (!legacy && pd.k <= kIncMaxK && !inc_off) {
       // sparse incidence kernel (lp_hist_inc.cu)
       const int km = kmax_for(pd.k);
       int e = pd.entry_base;
@@ -491,7 +540,10 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   if (e != cudaSuccess) return e;
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 3)
+    if (g.kind == 4)
+      e = launch_hist_rows(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
+                           d.draws, d.binom, d.evt, d.h0);
+    else if (g.kind == 3)
       e = launch_hist_inc(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
                           d.draws, d.binom, d.divtab, d.evt, d.h0);
     else if (g.kind == 2)

@@ -1,0 +1,248 @@
+// lp_hist_rows.cu — K1 v4: bit-sliced row resolution (sm_100a), k-independent.
+//
+// For depth P the slots of a scenario form a Dmax x P grid (row x = pipeline,
+// column = stage); a config (D, P) owns rows 0..D-1.  Instead of visiting the
+// k preempted slots once per depth, a thread walks the Dmax rows of its
+// scenario's slot bitmap, each row a P-bit vector pulled out of the bitmap
+// with funnel shifts, and keeps the per-stage preemption counts as B
+// bit-planes (a vertical binary counter per stage, B = bits(tmax)):
+//
+//   hit  = R & (count == max)          (B LOP3 per word)
+//   if hit != 0: event (t = max + 1, x); max++
+//   count += R                         (ripple carry, 2B ops per word)
+//
+// so a depth costs Dmax * ceil(P/32) * (3B + 4) integer ops, independent of
+// how many slots were preempted.  All lanes of a warp walk the same depth,
+// the same rows and the same plane count: the loop has no divergence; only
+// the (rare) event RED.ADD is predicated.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lp_device.cuh"
+#include "lp_layout.h"
+
+namespace lp {
+namespace {
+
+__device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <typename T>
+__device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
+  T* r = reinterpret_cast<T*>(p);
+  p += a16(count * sizeof(T));
+  return r;
+}
+
+template <bool SMEM_EVT>
+__device__ __forceinline__ void evt_add(uint32_t* a) {
+  if (SMEM_EVT) {
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(a)))
+                 : "memory");
+  } else {
+    atomicAdd(a, 1u);
+  }
+}
+
+// Walk the rows of one depth.  BMc: this thread's bitmap column (stride T),
+// with at least one zero word past the last slot word.
+template <int W, int B, bool SMEM_EVT>
+__device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P, int Dm,
+                                          uint32_t* eb) {
+  uint32_t C[B][W];
+#pragma unroll
+  for (int l = 0; l < B; ++l)
+#pragma unroll
+    for (int w = 0; w < W; ++w) C[l][w] = 0u;
+  const uint32_t tail = P - 32u * (W - 1);  // bits in the last word (1..32)
+  const uint32_t tmask = tail >= 32u ? 0xffffffffu : ((1u << tail) - 1u);
+  uint32_t mx = 0;
+  uint32_t pos = 0;
+  for (int x = 0; x < Dm; ++x, pos += P) {
+    const uint32_t wi = pos >> 5, sh = pos & 31u;
+    uint32_t R[W];
+    uint32_t lo = BMc[wi * T];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t hi = BMc[(wi + w + 1) * T];
+      R[w] = __funnelshift_r(lo, hi, sh);
+      lo = hi;
+    }
+    R[W - 1] &= tmask;
+    // positions at count == mx that this row hits
+    uint32_t hit = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint32_t eq = R[w];
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        const uint32_t m = ((mx >> l) & 1u) ? 0u : 0xffffffffu;  // select C or ~C
+        eq &= C[l][w] ^ m;
+      }
+      hit |= eq;
+    }
+    if (hit) {
+      ++mx;
+      if (mx >= 2u) evt_add<SMEM_EVT>(eb + (static_cast<int>(mx) - 2) * Dm + x);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint32_t carry = R[w];
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        const uint32_t t = C[l][w] & carry;
+        C[l][w] ^= carry;
+        carry = t;
+      }
+    }
+  }
+}
+
+template <int W, bool SMEM_EVT>
+__device__ __forceinline__ void walk_rows_b(int b, const uint32_t* BMc, int T, uint32_t P, int Dm,
+                                            uint32_t* eb) {
+  switch (b) {
+    case 2: walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 3: walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 4: walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 5: walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 6: walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 7: walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    default: walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+  }
+}
+
+}  // namespace
+
+template <int KREG, bool SMEM_EVT>
+__global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __restrict__ work,
+                                                           const PairDesc* __restrict__ pairs,
+                                                           const EntryDesc* __restrict__ entries,
+                                                           const DrawConst* __restrict__ draws,
+                                                           const uint64_t* __restrict__ binom,
+                                                           uint32_t* __restrict__ evt_g,
+                                                           uint32_t* __restrict__ h0_g) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  const WorkItem w = work[blockIdx.x];
+  const PairDesc pd = pairs[w.pair];
+  const int ne = w.e_res_hi - w.e_lo;
+  const int k = pd.k, n = pd.n;
+  const int nw = (n + 31) >> 5;
+  const bool own_h0 = (w.e_lo == pd.entry_base);
+
+  unsigned char* p = smem;
+  EntryDesc* ents = carve<EntryDesc>(p, ne > 0 ? ne : 1);
+  DrawConst* dc = carve<DrawConst>(p, k > 0 ? k : 1);
+  uint32_t* h0 = carve<uint32_t>(p, n);
+  uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, w.evt_len) : nullptr;
+  uint32_t* BM = carve<uint32_t>(p, static_cast<size_t>(nw + 1) * T);  // +1 zero word
+  uint32_t* MAP = (KREG == 0) ? carve<uint32_t>(p, static_cast<size_t>(k > 0 ? k : 1) * T) : nullptr;
+  uint16_t* SS = (KREG == 0) ? carve<uint16_t>(p, static_cast<size_t>(k > 0 ? k : 1) * T) : nullptr;
+
+  for (int i = tid; i < ne; i += T) {
+    EntryDesc e = entries[w.e_lo + i];
+    if (SMEM_EVT) e.evt_off -= w.evt_lo;
+    ents[i] = e;
+  }
+  if (!pd.exact)
+    for (int i = tid; i < k; i += T) dc[i] = draws[pd.draw_off + i];
+  for (int i = tid; i < n; i += T) h0[i] = 0u;
+  if (SMEM_EVT)
+    for (int i = tid; i < w.evt_len; i += T) evt[i] = 0u;
+  __syncthreads();
+  uint32_t* evt_base = SMEM_EVT ? evt : evt_g;
+  uint32_t* BMc = BM + tid;
+
+  for (uint64_t t = w.t0 + tid; t < w.t1; t += T) {
+    uint32_t s0 = 0;
+    if (KREG > 0 && !pd.exact) {
+      uint32_t s[KREG > 0 ? KREG : 1];
+      gen_mc_regs<(KREG > 0 ? KREG : 1)>(pd.seed, t, k, dc, s);
+      for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
+#pragma unroll
+      for (int j = 0; j < (KREG > 0 ? KREG : 1); ++j)
+        if (j < k) BMc[(s[j] >> 5) * T] |= 1u << (s[j] & 31);
+      s0 = s[0];
+    } else if (pd.exact) {
+      // unrank into the bitmap directly
+      for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
+      uint64_t rank = t;
+      int c = 0;
+      for (int i = 0; i < k; ++i) {
+        const int rem = k - i - 1;
+        while (true) {
+          const uint64_t num = binom_at(binom + pd.binom_off, pd.binom_stride, n - c - 1, rem);
+          if (rank < num) break;
+          rank -= num;
+          ++c;
+        }
+        if (i == 0) s0 = static_cast<uint32_t>(c);
+        BMc[(c >> 5) * T] |= 1u << (c & 31);
+        ++c;
+      }
+    } else {
+      gen_mc_generic(pd.seed, t, n, k, dc, MAP + tid, T, BMc, T, SS + tid, T);
+      BMc[nw * T] = 0u;
+      s0 = SS[tid];
+    }
+    if (own_h0 && k > 0) atomicAdd(&h0[s0], 1u);
+
+    for (int ei = 0; ei < ne; ++ei) {
+      const EntryDesc e = ents[ei];
+      const uint32_t P = static_cast<uint32_t>(e.P);
+      const int Dm = e.Dmax;
+      const int b = 32 - __clz(static_cast<uint32_t>(e.tmax));  // bits of tmax (>= 2)
+      uint32_t* eb = evt_base + e.evt_off;
+      switch ((P + 31u) >> 5) {
+        case 1: walk_rows_b<1, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 2: walk_rows_b<2, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 3: walk_rows_b<3, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 4: walk_rows_b<4, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 5: walk_rows_b<5, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 6: walk_rows_b<6, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 7: walk_rows_b<7, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        default: walk_rows_b<8, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+      }
+    }
+  }
+  __syncthreads();
+  if (own_h0)
+    for (int i = tid; i < n; i += T)
+      if (h0[i]) atomicAdd(&h0_g[pd.h0_off + i], h0[i]);
+  if (SMEM_EVT)
+    for (int i = tid; i < w.evt_len; i += T)
+      if (evt[i]) atomicAdd(&evt_g[w.evt_lo + i], evt[i]);
+}
+
+template <int KREG, bool SM>
+static cudaError_t launch_rows_t(int blocks, int threads, size_t smem, cudaStream_t st,
+                                 const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
+                                 const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
+                                 uint32_t* h0) {
+  auto fn = hist_rows_kernel<KREG, SM>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, evt, h0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_rows(int kreg, bool smem_evt, int blocks, int threads, size_t smem,
+                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
+                             const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
+                             uint32_t* evt, uint32_t* h0) {
+  if (blocks <= 0) return cudaSuccess;
+#define LP_W(K)                                                                                   \
+  if (kreg == K)                                                                                  \
+    return smem_evt ? launch_rows_t<K, true>(blocks, threads, smem, st, w, pairs, ents, dr, binom, \
+                                             evt, h0)                                             \
+                    : launch_rows_t<K, false>(blocks, threads, smem, st, w, pairs, ents, dr,      \
+                                              binom, evt, h0);
+  LP_W(0)
+  LP_W(16)
+#undef LP_W
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lp
