@@ -54,7 +54,7 @@ def distinct_pairs(n_seq):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons DURING the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -62,6 +62,13 @@ class ClockSampler:
         self.device = device
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __enter__(self):
         try:
@@ -76,7 +83,7 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")][1:]))
 
     def __exit__(self, *a):
         if self.proc:
@@ -87,6 +94,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        rows = [r for ts, r in self.rows if self.t0 is None or (self.t0 <= ts <= (self.t1 or ts) + 0.15)]
+        if not rows:
+            rows = [r for ts, r in self.rows]
+        self_rows = self.rows
+        self.rows = rows
+        try:
+            return self._summary()
+        finally:
+            self.rows = self_rows
+
+    def _summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
@@ -117,32 +135,56 @@ def load_profile_traffic():
     return None
 
 
-def cpu_reference_sample(n_seq, current, target_s=12.0, threads=None):
+class RefArm:
     """The reference's own survivor-histogram path (Planner::phi ->
-    survivor_histogram) on all host cores over a bounded sample: every MC pair
-    of the workload at a reduced trial count.  Returns (value, info)."""
-    import ctypes as C
-    from oracle.oracle import ref_lib
-    from paper_2403_14097_b200.model import CostTable, PlannerOptions, PROFILES
-    L = ref_lib()
-    w = PROFILES[PROFILE]()
-    threads = threads or os.cpu_count() or 1
-    pairs = distinct_pairs(n_seq)
-    pn = (C.c_int * len(pairs))(*[p[0] for p in pairs])
-    pk = (C.c_int * len(pairs))(*[p[1] for p in pairs])
-    prof, keep = w.to_c()
-    costs = CostTable().to_c()
-    trials = 50
-    res = C.c_ulonglong()
-    while True:
+    survivor_histogram, optimizer.cpp:52-94) on all host cores over a bounded
+    sample: every (n, k) ensemble of the workload at a reduced trial count
+    (resolutions/s does not depend on the trial count)."""
+
+    def __init__(self, n_seq, threads=None):
+        import ctypes as C
+        from oracle.oracle import ref_lib
+        from paper_2403_14097_b200.model import CostTable, PROFILES
+        self.C = C
+        self.L = ref_lib()
+        self.threads = threads or os.cpu_count() or 1
+        self.pairs = distinct_pairs(n_seq)
+        self.pn = (C.c_int * len(self.pairs))(*[p[0] for p in self.pairs])
+        self.pk = (C.c_int * len(self.pairs))(*[p[1] for p in self.pairs])
+        self.prof, self.keep = PROFILES[PROFILE]().to_c()
+        self.costs = CostTable().to_c()
+        self.trials = 50
+
+    def run(self, trials):
+        from paper_2403_14097_b200.model import PlannerOptions
+        C = self.C
         opt = PlannerOptions(mc_trials=trials).to_c()
-        secs = L.ref_bench_histograms(C.byref(prof), C.byref(costs), C.byref(opt), pn, pk, len(pairs), threads,
-                                      C.byref(res))
-        if secs >= target_s / 4 or trials >= 1_000_000:
-            break
-        trials = int(min(1_000_000, trials * max(2.0, min(8.0, target_s / 4 / max(secs, 1e-3)))))
-    return res.value / secs, {"trials_per_point": trials, "seconds": secs, "resolutions": res.value,
-                              "threads": threads, "pairs": len(pairs)}
+        res = C.c_ulonglong()
+        secs = self.L.ref_bench_histograms(C.byref(self.prof), C.byref(self.costs), C.byref(opt), self.pn, self.pk,
+                                           len(self.pairs), self.threads, C.byref(res))
+        return res.value, secs
+
+    def calibrate(self, step_s):
+        while True:
+            res, secs = self.run(self.trials)
+            if secs >= step_s / 2 or self.trials >= 1_000_000:
+                break
+            self.trials = int(min(1_000_000, self.trials * max(2.0, min(8.0, step_s / max(secs, 1e-3)))))
+        return self
+
+    def info(self):
+        return (f"all {len(self.pairs)} (n,k) ensembles of the workload at {self.trials} trials/point "
+                f"instead of the workload's trial count, {self.threads} threads")
+
+
+def cpu_reference_sample(n_seq, target_s=6.0):
+    arm = RefArm(n_seq).calibrate(target_s / 3)
+    tot_r, tot_s = 0, 0.0
+    while tot_s < target_s:
+        r, s_ = arm.run(arm.trials)
+        tot_r += r
+        tot_s += s_
+    return tot_r / tot_s, arm
 
 
 def run_reference(args):
@@ -155,21 +197,23 @@ def run_reference(args):
         from oracle.oracle import REF_LIB
         if not REF_LIB.exists():
             raise FileNotFoundError(str(REF_LIB))
-        vals = []
-        info = None
+        # each step: one bounded sample sized so the whole run ends within minutes
+        step_s = max(0.25, min(3.0, 120.0 / max(1, steps + warm)))
+        arm = RefArm(n_seq).calibrate(step_s)
+        tot_r, tot_s = 0, 0.0
         for i in range(warm + steps):
-            v, info = cpu_reference_sample(n_seq, None, target_s=args.ref_seconds)
+            r, s_ = arm.run(arm.trials)
             if i >= warm:
-                vals.append(v)
-        value = statistics.mean(vals)
+                tot_r += r
+                tot_s += s_
+        value = tot_r / tot_s
         line = {"impl": "reference", "metric": "liveput scenarios/sec", "value": value, "unit": "resolutions/s",
                 "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
-                "ms_per_step": info["seconds"] * 1000.0, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64",
+                "ms_per_step": tot_s * 1000.0 / steps, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64",
                 "data": "synthetic availability sequence (no dataset)",
                 "config": workload_config(args, n_seq),
-                "cpu_baseline": {"value": value, "unit": "resolutions/s", "cores": info["threads"], "kind": "reference",
-                                 "sample": f"all {info['pairs']} (n,k) ensembles of the workload at "
-                                           f"{info['trials_per_point']} trials/point instead of {args.trials}"},
+                "cpu_baseline": {"value": value, "unit": "resolutions/s", "cores": arm.threads, "kind": "reference",
+                                 "sample": arm.info()},
                 "e2e": {"value": value, "unit": "resolutions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     except Exception as e:  # pragma: no cover
         line = {"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}
@@ -188,13 +232,13 @@ def workload_config(args, n_seq):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--instances", type=int, default=256)
     ap.add_argument("--lookahead", type=int, default=24)
     ap.add_argument("--trials", type=int, default=1_000_000)
-    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -248,6 +292,8 @@ def main():
     evs = []
     hist_ms, dp_ms, red_ms = [], [], []
     with ClockSampler(local) as clk:
+        time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
+        clk.mark_start()
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
@@ -262,6 +308,7 @@ def main():
             dp_ms.append(s.dp_ms)
             red_ms.append(s.reduce_ms)
         barrier()
+        clk.mark_end()
     dev_ms = sum(a.elapsed_time(b) for a, b in evs)
     dev_ms = max_over_ranks(dev_ms)
     st = pl.stats()
@@ -319,11 +366,9 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            v, info = cpu_reference_sample(n_seq, current, target_s=args.ref_seconds)
-            line["cpu_baseline"] = {"value": v, "unit": "resolutions/s", "cores": info["threads"], "kind": "reference",
-                                    "sample": f"reference Planner survivor histograms of all {info['pairs']} (n,k) "
-                                              f"ensembles at {info['trials_per_point']} trials/point "
-                                              f"({info['seconds']:.1f} s on {info['threads']} threads)"}
+            v, arm = cpu_reference_sample(n_seq, target_s=args.ref_seconds)
+            line["cpu_baseline"] = {"value": v, "unit": "resolutions/s", "cores": arm.threads, "kind": "reference",
+                                    "sample": "reference Planner::survivor_histogram over " + arm.info()}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)
