@@ -195,7 +195,7 @@ uint64_t alg_ops(uint64_t scen, int k, int depths) {
 }
 
 lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int nranks,
-                          HistPlan& hp, std::string& err) {
+                          HistPlan& hp, std::string& err, int num_sms = 148) {
   hp = HistPlan();
   for (const EnsembleSpec& sp : specs) {
     const int n = sp.n, k = sp.k;
@@ -278,6 +278,13 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     hp.alg_ops += alg_ops(local, k, pd.n_entries);
   }
 
+  // scenarios per block: enough blocks for ~12 per SM over all ensembles (so
+  // trial-sharded ranks keep every SM busy), at most 16 per thread
+  uint64_t local_total = 0;
+  for (const PairDesc& pd : hp.pairs) local_total += pd.t_hi - pd.t_lo;
+  const uint64_t want_blocks = (uint64_t)std::max(num_sms, 1) * 12;
+  const uint64_t per_block = std::min<uint64_t>(4096, std::max<uint64_t>(256, ((local_total / want_blocks) + 255) & ~255ull));
+
   // work items, grouped by launch configuration
   std::map<std::tuple<int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
   const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
@@ -310,7 +317,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         int T = 256;
         while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg);
-        const uint64_t chunk = (uint64_t)T * 16;
+        const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -352,7 +359,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         int T = 128;
         while (T > 32 && smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T) > kSmemBudgetInc) T >>= 1;
         const size_t smem = smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T);
-        const uint64_t chunk = (uint64_t)T * 16;
+        const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -399,7 +406,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         int T = 256;
         while (T > 32 && smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
-        const uint64_t chunk = (uint64_t)T * 16;
+        const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -624,6 +631,7 @@ struct lp_handle {
   lp_options opt{};
   CostScalars cs{};
   int device = 0;
+  int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   std::string err;
@@ -857,6 +865,7 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = h;
   return LP_OK;
 }
@@ -955,7 +964,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     specs[spec_of[{std::get<2>(kk), std::get<3>(kk)}]].ref_keys++;
   }
   std::string err;
-  lp_status s = build_hist_plan(specs, h->rank, h->nranks, h->hp, err);
+  lp_status s = build_hist_plan(specs, h->rank, h->nranks, h->hp, err, h->num_sms);
   if (s != LP_OK) return fail(h, s, "%s", err.c_str());
   // node histogram rows + levels
   std::map<int, int> thr_need;
