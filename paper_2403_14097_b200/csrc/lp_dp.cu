@@ -130,7 +130,10 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 }
 
 // F_{j+1}[c'] = max_c F_j[c] + phi(c, c') with the reference's tie rules.
-__global__ void __launch_bounds__(256) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
+// One block per next-level node; threads stride over the prev nodes (each
+// keeps the first best in its own ascending order), then a warp-shuffle and a
+// cross-warp reduction pick (value desc, mig asc, index asc).
+__global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
                                                       const NodeCfg* __restrict__ cfg,
                                                       const NodeCost* __restrict__ cost,
                                                       const uint32_t* __restrict__ hist,
@@ -141,15 +144,15 @@ __global__ void __launch_bounds__(256) dp_step_kernel(int j, const LevelDesc* __
                                                       int32_t* __restrict__ parent,
                                                       double* __restrict__ stc,
                                                       double* __restrict__ stm) {
+  __shared__ Cand s_best[4];
   const LevelDesc L = levels[j];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= L.next_count) return;
-  const int ni = L.next_base + warp;
+  if (static_cast<int>(blockIdx.x) >= L.next_count) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ni = L.next_base + blockIdx.x;
   const NodeCfg nx = cfg[ni];
   const NodeCost nc = cost[ni];
   Cand best{0.0, 0.0, 0.0, 0.0, -1};
-  for (int pi = lane; pi < L.prev_count; pi += 32) {
+  for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
     const int gi = L.prev_base + pi;
     const NodeCfg pv = cfg[gi];
     const PhiOut ph = phi_dev(pv, nx, nc, L, S, hist, thr_tab, thr_row);
@@ -168,7 +171,11 @@ __global__ void __launch_bounds__(256) dp_step_kernel(int j, const LevelDesc* __
     const Cand o = shfl_cand(best, lane ^ off);
     if (cand_better(o, best)) best = o;
   }
-  if (lane == 0) {
+  if (lane == 0) s_best[warp] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (cand_better(s_best[w], best)) best = s_best[w];
     val[ni] = best.value;
     mig[ni] = best.mig;
     parent[ni] = best.idx;
@@ -285,11 +292,9 @@ cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDe
                            const NodeCfg* cfg, const NodeCost* cost, const uint32_t* hist,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm) {
-  const int threads = 256;
-  const int warps_per_block = threads / 32;
-  const int blocks = (next_count + warps_per_block - 1) / warps_per_block;
+  const int blocks = next_count;
   if (blocks <= 0) return cudaSuccess;
-  dp_step_kernel<<<blocks, threads, 0, st>>>(j, levels, cfg, cost, hist, thr_tab, thr_row, S, val,
+  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, cost, hist, thr_tab, thr_row, S, val,
                                              mig, parent, stc, stm);
   return cudaGetLastError();
 }
