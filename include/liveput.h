@@ -115,6 +115,7 @@ typedef struct {
   uint64_t hist_alg_ops;     /* algorithmic int32-equivalent ops of the histogram kernel */
   uint64_t h2d_bytes;        /* bytes copied host->device by the last prepare */
   uint64_t d2h_bytes;        /* bytes copied device->host by the last fetch */
+  double prepare_ms;         /* host wall time of the last lp_prepare (tables + H2D issue) */
 } lp_stats;
 
 typedef struct lp_handle lp_handle;

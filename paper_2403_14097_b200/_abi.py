@@ -91,6 +91,7 @@ class lp_stats(C.Structure):
         ("hist_alg_ops", C.c_uint64),
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
+        ("prepare_ms", C.c_double),
     ]
 
 

@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -80,6 +81,7 @@ struct PinBuf {
 // Sections appended to one host image and uploaded with a single copy.
 struct Packer {
   std::vector<unsigned char> bytes;
+  Packer() { bytes.reserve(1 << 21); }
   size_t add(const void* src, size_t n) {
     size_t off = (bytes.size() + 255) & ~size_t(255);
     bytes.resize(off + std::max<size_t>(n, 1));
@@ -582,7 +584,7 @@ void build_thr(Model& m, const std::map<int, int>& need, int pmax, ThrTable& t) 
   t.vals.clear();
   for (const auto& [P, Dm] : need) {
     t.row[P] = (int32_t)t.vals.size();
-    for (int D = 0; D <= Dm; ++D) t.vals.push_back(D == 0 ? 0.0 : m.rate(D, P));
+    for (int D = 0; D <= Dm; ++D) t.vals.push_back(D == 0 ? 0.0 : m.rate_cached(D, P));
   }
 }
 
@@ -810,7 +812,7 @@ lp_status planner_rows(lp_handle* h, int D, int P, int n, int k, std::vector<uin
 NodeCost node_cost(lp_handle* h, int d, int p) {
   NodeCost c{};
   if (d <= 0) return c;
-  c.thr = h->model.rate(d, p);
+  c.thr = h->model.rate_cached(d, p);
   c.pipe = h->model.pipe_transfer(p);
   c.unit = h->model.inter_unit(p);
   // resume_cost (migration.cpp:100-104)
@@ -893,6 +895,7 @@ void* lp_stream(lp_handle* h) { return h ? (void*)h->stream : nullptr; }
 // prepare: levels (optimizer.cpp:148-183), ensembles, tables; one H2D copy.
 lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len) {
   if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  const auto t_start = std::chrono::steady_clock::now();
   if (!n_seq || len < 2) return fail(h, LP_EINVAL, "dp_optimize: need at least N_i and N_{i+1}");
   cudaSetDevice(h->device);
   for (int i = 0; i < len; ++i) {
@@ -1065,6 +1068,8 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->stats.horizon = H;
   h->stats.hist_alg_ops = h->hp.alg_ops;
   h->stats.h2d_bytes = pk.bytes.size() + sizeof(int32_t) * len;
+  h->stats.prepare_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return LP_OK;
 }
 

@@ -59,6 +59,14 @@ double Model::rate(int d, int p) const {
   return static_cast<double>(batch) / (pipe_s + grad_sync);
 }
 
+double Model::rate_cached(int d, int p) {
+  if (p < 1 || d < 1) return rate(d, p);
+  if (static_cast<int>(rate_cache_.size()) <= p) rate_cache_.resize(p + 1);
+  std::vector<double>& row = rate_cache_[p];
+  while (static_cast<int>(row.size()) <= d) row.push_back(rate(static_cast<int>(row.size()), p));
+  return row[d];
+}
+
 const std::vector<Cfg>& Model::configs(int n) {
   static const std::vector<Cfg> kEmpty;
   if (n <= 0) return kEmpty;

@@ -27,6 +27,8 @@ class Model {
   bool depth_ok(int stages) const;
   // perf_model.cpp:14-42 (+ microbatches_per_pipeline, perf_model.hpp:44-48)
   double rate(int d, int p) const;
+  // memoised rate(d, p): the profile is fixed for the life of a handle
+  double rate_cached(int d, int p);
   // perf_model.cpp:44-52 — ascending P, descending D (fixes DP tie order)
   const std::vector<Cfg>& configs(int n);
   // optimizer.cpp:11-25
@@ -43,6 +45,7 @@ class Model {
   std::vector<int32_t> depths_;
   std::vector<double> rates_;
   std::vector<std::vector<Cfg>> cfg_cache_;
+  std::vector<std::vector<double>> rate_cache_;  // [p][d]
   std::vector<char> cfg_have_;
   bool lookup_rate(int p, double* r) const;
 };

@@ -33,10 +33,16 @@ def main():
         t = time.perf_counter()
         p.execute()
         s = p.stats()
-        print(f"{a.case}: total {s.total_ms:.3f} ms hist {s.hist_ms:.3f} dp {s.dp_ms:.3f} "
+        print(f"{a.case}: total {s.total_ms:.3f} ms hist {s.hist_ms:.3f} dp {s.dp_ms:.3f} prep {s.prepare_ms:.3f} "
               f"res {s.resolutions} scen {s.scenarios} launches {s.kernel_launches} "
               f"wall {1e3 * (time.perf_counter() - t):.2f} ms", flush=True)
     plan = p.fetch(len(ns) - 1)
+    for _ in range(3):  # end to end through lp_replan (host tables + H2D + kernels + D2H)
+        t = time.perf_counter()
+        p.dp_optimize(cur, ns)
+        s = p.stats()
+        print(f"{a.case}: e2e {1e3 * (time.perf_counter() - t):.3f} ms (prepare {s.prepare_ms:.3f} ms, "
+              f"h2d {s.h2d_bytes} B)", flush=True)
     print([(x.config.pipelines, x.config.stages) if x.config else None for x in plan])
     p.close()
 
