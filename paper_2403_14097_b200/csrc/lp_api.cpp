@@ -646,7 +646,7 @@ struct lp_handle {
   HistPlan hp;
   std::vector<LevelDesc> levels;
   std::vector<NodeCfg> cfg;
-  std::vector<NodeCost> cost;
+  std::vector<double4> pcost;  // per depth: pipe transfer, inter unit, resume cost
   std::vector<int4> lrows;
   ThrTable thr;
   DpScalars S{};
@@ -914,33 +914,31 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->horizon = H;
   h->levels.assign(H, LevelDesc{});
   h->cfg.clear();
-  h->cost.clear();
   std::vector<int> lbase(H + 1), lcount(H + 1);
   // level 0: current
   lbase[0] = 0;
   lcount[0] = 1;
   h->cfg.push_back({cur_on ? current.pipelines : 0, cur_on ? current.stages : 0, -1, 0});
-  h->cost.push_back(NodeCost{});
   for (int j = 1; j <= H; ++j) {
     lbase[j] = (int)h->cfg.size();
     for (const Cfg& c : h->model.configs(n_seq[j])) {
       h->cfg.push_back({c.d, c.p, -1, 0});
-      h->cost.push_back(node_cost(h, c.d, c.p));
     }
     h->cfg.push_back({0, 0, -1, 0});  // suspension is always reachable
-    h->cost.push_back(NodeCost{});
     lcount[j] = (int)h->cfg.size() - lbase[j];
   }
-  // ensembles: one per distinct (n_now, k) whose histograms phi will read
+  // ensembles: one per distinct (n_now, k) whose histograms phi will read.
+  // Level j >= 1 needs every config of n_now (all D <= n/P of each feasible
+  // P); level 0 needs only `current`.
   std::map<std::pair<int, int>, int> spec_of;
   std::vector<EnsembleSpec> specs;
+  std::vector<char> spec_full;             // some level j >= 1 uses the spec
+  std::vector<std::pair<int, int>> spec_cur;  // (D, P) of current when level 0 uses it
   std::vector<int> level_spec(H, -1);
-  std::map<std::tuple<int, int, int, int>, char> keys;  // reference hist keys (D,P,n,k)
   for (int j = 0; j < H; ++j) {
     const int n_now = n_seq[j], n_next = n_seq[j + 1];
     const int k = std::max(0, n_now - n_next);
-    bool any_prev = false;
-    for (int i = 0; i < lcount[j]; ++i) any_prev |= h->cfg[lbase[j] + i].d > 0;
+    const bool any_prev = (j == 0) ? cur_on : !h->model.configs(n_now).empty();
     const bool any_next = !h->model.configs(n_next).empty();
     if (!any_prev || !any_next) continue;
     auto key = std::make_pair(n_now, k);
@@ -951,20 +949,36 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
       if (s != LP_OK) return s;
       it = spec_of.emplace(key, (int)specs.size()).first;
       specs.push_back(sp);
+      spec_full.push_back(0);
+      spec_cur.push_back({0, 0});
     }
-    EnsembleSpec& sp = specs[it->second];
-    for (int i = 0; i < lcount[j]; ++i) {
-      const NodeCfg& c = h->cfg[lbase[j] + i];
-      if (c.d <= 0) continue;
-      int& dm = sp.dmax_by_p[c.p];
-      dm = std::max(dm, j == 0 ? c.d : n_now / c.p);
-      keys[{c.d, c.p, n_now, k}] = 1;
+    const int si = it->second;
+    EnsembleSpec& sp = specs[si];
+    if (j == 0) {
+      int& dm = sp.dmax_by_p[current.stages];
+      dm = std::max(dm, current.pipelines);
+      spec_cur[si] = {current.pipelines, current.stages};
+    } else if (!spec_full[si]) {
+      spec_full[si] = 1;
+      int last_p = -1;
+      for (const Cfg& c : h->model.configs(n_now))  // ascending P, first D of a P = n/P
+        if (c.p != last_p) {
+          int& dm = sp.dmax_by_p[c.p];
+          dm = std::max(dm, c.d);
+          last_p = c.p;
+        }
     }
-    level_spec[j] = it->second;
+    level_spec[j] = si;
   }
-  for (const auto& [kk, v] : keys) {
-    (void)v;
-    specs[spec_of[{std::get<2>(kk), std::get<3>(kk)}]].ref_keys++;
+  // distinct (D, P, n, k) histogram keys the reference would tally
+  for (size_t si = 0; si < specs.size(); ++si) {
+    uint64_t keys = spec_full[si] ? h->model.configs(specs[si].n).size() : 0;
+    const auto [cd, cp] = spec_cur[si];
+    if (cd > 0) {
+      const bool covered = spec_full[si] && h->model.depth_ok(cp) && cd <= specs[si].n / cp;
+      if (!covered) keys += 1;
+    }
+    specs[si].ref_keys = keys;
   }
   std::string err;
   lp_status s = build_hist_plan(specs, h->rank, h->nranks, h->hp, err, h->num_sms);
@@ -972,6 +986,8 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   // node histogram rows + levels
   std::map<int, int> thr_need;
   int pmax = 1;
+  std::vector<int> entry_of_p;  // per pair: depth -> entry index
+  std::vector<int> need_d;      // per depth: largest D read from the throughput table
   for (int j = 0; j < H; ++j) {
     LevelDesc& L = h->levels[j];
     L.n_now = n_seq[j];
@@ -987,25 +1003,38 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     if (!L.has_hist) continue;
     const PairDesc& pd = h->hp.pairs[level_spec[j]];
     L.total = pd.count;
+    entry_of_p.assign(pd.n + 2, -1);
+    for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
+      entry_of_p[h->hp.entries[e].P] = e;
     for (int i = 0; i < lcount[j]; ++i) {
       NodeCfg& c = h->cfg[lbase[j] + i];
       if (c.d <= 0) continue;
-      for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
-        if (h->hp.entries[e].P == c.p) c.hist_off = h->hp.entries[e].hist_off + hist_row(c.d, L.k);
-      int& dm = thr_need[c.p];
-      dm = std::max(dm, c.d);
-      pmax = std::max(pmax, c.p);
+      const int e = entry_of_p[c.p];
+      if (e >= 0) c.hist_off = h->hp.entries[e].hist_off + hist_row(c.d, L.k);
+      if ((int)need_d.size() <= c.p) need_d.resize(c.p + 1, 0);
+      need_d[c.p] = std::max(need_d[c.p], c.d);
     }
   }
-  if (h->opt.strict_conditional)
-    for (int j = 1; j <= H; ++j)
-      for (int i = 0; i < lcount[j]; ++i) {
-        const NodeCfg& c = h->cfg[lbase[j] + i];
-        if (c.d <= 0) continue;
-        int& dm = thr_need[c.p];
-        dm = std::max(dm, c.d);
-        pmax = std::max(pmax, c.p);
-      }
+  // next-role nodes: throughput(next) (and thr(alive, P) when strict) and
+  // the per-depth cost terms
+  for (int j = 1; j <= H; ++j)
+    for (int i = 0; i < lcount[j]; ++i) {
+      const NodeCfg& c = h->cfg[lbase[j] + i];
+      if (c.d <= 0) continue;
+      if ((int)need_d.size() <= c.p) need_d.resize(c.p + 1, 0);
+      need_d[c.p] = std::max(need_d[c.p], c.d);
+    }
+  h->pcost.assign(need_d.size() + 1, make_double4(0.0, 0.0, 0.0, 0.0));
+  for (int p = 1; p < (int)need_d.size(); ++p)
+    if (need_d[p] > 0) {
+      const NodeCost nc = node_cost(h, 1, p);
+      h->pcost[p] = make_double4(nc.pipe, nc.unit, nc.resume, 0.0);
+    }
+  for (int p = 1; p < (int)need_d.size(); ++p)
+    if (need_d[p] > 0) {
+      thr_need[p] = need_d[p];
+      pmax = std::max(pmax, p);
+    }
   build_thr(h->model, thr_need, pmax, h->thr);
   // liveput rows
   h->lrows.clear();
@@ -1028,7 +1057,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->off_divtab = pk.add(h->hp.divtab);
   h->off_levels = pk.add(h->levels);
   h->off_cfg = pk.add(h->cfg);
-  h->off_cost = pk.add(h->cost);
+  h->off_cost = pk.add(h->pcost);
   h->off_lrows = pk.add(h->lrows);
   h->off_thr = pk.add(h->thr.vals);
   h->off_throw = pk.add(h->thr.row);
@@ -1100,7 +1129,7 @@ lp_status lp_execute(lp_handle* h) {
   LP_CUDA(h, cudaEventRecord(h->ev[2], st));
   const LevelDesc* lv = dptr<LevelDesc>(h->tables, h->off_levels);
   const NodeCfg* cfg = dptr<NodeCfg>(h->tables, h->off_cfg);
-  const NodeCost* cost = dptr<NodeCost>(h->tables, h->off_cost);
+  const double4* pcost = dptr<double4>(h->tables, h->off_cost);
   const double* thr = dptr<double>(h->tables, h->off_thr);
   const int32_t* throw_ = dptr<int32_t>(h->tables, h->off_throw);
   double* val = dptr<double>(h->work, h->w_val);
@@ -1111,7 +1140,7 @@ lp_status lp_execute(lp_handle* h) {
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
   for (int j = 0; j < h->horizon; ++j) {
-    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, cost, d.hist, thr, throw_,
+    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, pcost, d.hist, thr, throw_,
                               h->S, val, mig, par, stc, stm));
     ++launches;
   }

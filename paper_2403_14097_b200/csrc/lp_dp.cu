@@ -11,10 +11,10 @@
 // reference's x86-64 build has no FMA).  Probabilities are
 // count_m / count exactly as the reference's normalised histogram.
 //
-// Layout: one warp per next-level node; lanes stride over prev nodes; the
-// (value desc, mig asc, first index) argmax is a warp shuffle reduction.  The
-// winning value, migration total, back-pointer and step terms of every node
-// stay in HBM for the traceback.
+// Layout: one block per next-level node; threads stride over prev nodes; the
+// (value desc, mig asc, first index) argmax is a warp-shuffle + cross-warp
+// reduction.  The winning value, migration total, back-pointer and step terms
+// of every node stay in HBM for the traceback.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -135,7 +135,7 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 // cross-warp reduction pick (value desc, mig asc, index asc).
 __global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
                                                       const NodeCfg* __restrict__ cfg,
-                                                      const NodeCost* __restrict__ cost,
+                                                      const double4* __restrict__ pcost,
                                                       const uint32_t* __restrict__ hist,
                                                       const double* __restrict__ thr_tab,
                                                       const int32_t* __restrict__ thr_row,
@@ -150,7 +150,14 @@ __global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ni = L.next_base + blockIdx.x;
   const NodeCfg nx = cfg[ni];
-  const NodeCost nc = cost[ni];
+  NodeCost nc{0.0, 0.0, 0.0, 0.0};
+  if (nx.d > 0) {  // per-depth cost terms + throughput(next) from the tables
+    const double4 pc = pcost[nx.p];
+    nc.thr = thr_tab[thr_row[nx.p] + nx.d];
+    nc.pipe = pc.x;
+    nc.unit = pc.y;
+    nc.resume = pc.z;
+  }
   Cand best{0.0, 0.0, 0.0, 0.0, -1};
   for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
     const int gi = L.prev_base + pi;
@@ -289,12 +296,12 @@ __global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc
 
 // ---------------------------------------------------------------------------
 cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
-                           const NodeCfg* cfg, const NodeCost* cost, const uint32_t* hist,
+                           const NodeCfg* cfg, const double4* pcost, const uint32_t* hist,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm) {
   const int blocks = next_count;
   if (blocks <= 0) return cudaSuccess;
-  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, cost, hist, thr_tab, thr_row, S, val,
+  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, pcost, hist, thr_tab, thr_row, S, val,
                                              mig, parent, stc, stm);
   return cudaGetLastError();
 }
