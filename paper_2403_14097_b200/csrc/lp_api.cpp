@@ -177,8 +177,8 @@ size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T
   const size_t nw = (n + 31) / 32;
   const size_t kk = std::max(k, 1);
   return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(sizeof(DrawConst) * kk) +
-         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(4 * (nw + 1) * T) +
-         (kreg == 0 ? a16(4 * kk * T) + a16(2 * kk * T) : 0);
+         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) +
+         a16(4 * (nw + 1) * T) + (kreg == 0 ? a16(4 * kk * T) : 0);
 }
 
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {
@@ -308,14 +308,16 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (e2 < e_end) {
           const EntryDesc& x = hp.entries[e2];
           const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
-          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(4 * (size_t)ev2) > kScnFixedBudget)
+          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(2 * (size_t)ev2) > kScnFixedBudget)
             break;
           ev = ev2;
           ++e2;
         }
         int e_res = e;
-        while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
-        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(4 * (size_t)ev) <= kScnFixedBudget;
+        int pmax_res = 0;
+        while (e_res < e2 && hp.entries[e_res].tmax >= 2) pmax_res = std::max(pmax_res, hp.entries[e_res++].P);
+        const int wmax = pmax_res <= 128 ? 4 : 8;
+        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(2 * (size_t)ev) <= kScnFixedBudget;
         int T = 256;
         while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg);
@@ -331,7 +333,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.smem_evt = sm ? 1 : 0;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + chunk);
-          groups[{4, kreg, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
+          groups[{4, kreg * 16 + wmax, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
         }
         e = e2;
       }
@@ -550,8 +552,8 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
     if (g.kind == 4)
-      e = launch_hist_rows(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
-                           d.draws, d.binom, d.evt, d.h0);
+      e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+                           d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0);
     else if (g.kind == 3)
       e = launch_hist_inc(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
                           d.draws, d.binom, d.divtab, d.evt, d.h0);

@@ -101,6 +101,60 @@ __device__ __forceinline__ void gen_mc_regs(uint64_t seed, uint64_t t, int k, co
   sort_regs<KMAX>(s);
 }
 
+// Same draw, but only the selected set is kept: each slot is OR-ed into the
+// thread's bitmap column BMc[w * T] (zeroed by the caller) and the smallest
+// slot is returned.  The displacement map is packed (target << 16 | value)
+// in KMAX registers, so k up to 64 stays out of shared memory.
+template <int KMAX>
+__device__ __forceinline__ uint32_t gen_mc_bitmap(uint64_t seed, uint64_t t, int k,
+                                                  const DrawConst* dc, uint32_t* BMc, int T) {
+  uint64_t st = trial_state(seed, t);
+  uint32_t map[KMAX];
+  uint32_t smin = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i < k) {
+      const uint32_t j = static_cast<uint32_t>(i) + draw_below(st, dc[i]);
+      uint32_t vi = static_cast<uint32_t>(i), vj = j;
+#pragma unroll
+      for (int q = 0; q < i; ++q) {
+        const uint32_t tg = map[q] >> 16;
+        vi = (tg == static_cast<uint32_t>(i)) ? (map[q] & 0xffffu) : vi;
+        vj = (tg == j) ? (map[q] & 0xffffu) : vj;
+      }
+      const uint32_t sel = (j == static_cast<uint32_t>(i)) ? vi : vj;
+      map[i] = (j << 16) | vi;
+      BMc[(sel >> 5) * T] |= 1u << (sel & 31);
+      smin = min(smin, sel);
+    }
+  }
+  return smin;
+}
+
+// gen_mc_bitmap with the displacement map in a strided shared-memory column
+// (map[i * ms], any k): a compact loop instead of an unrolled one.
+__device__ __forceinline__ uint32_t gen_mc_bitmap_smem(uint64_t seed, uint64_t t, int k,
+                                                       const DrawConst* dc, uint32_t* map, int ms,
+                                                       uint32_t* BMc, int T) {
+  uint64_t st = trial_state(seed, t);
+  uint32_t smin = 0xffffffffu;
+  for (int i = 0; i < k; ++i) {
+    const uint32_t j = static_cast<uint32_t>(i) + draw_below(st, dc[i]);
+    uint32_t vi = static_cast<uint32_t>(i), vj = j;
+    for (int q = 0; q < i; ++q) {
+      const uint32_t e = map[q * ms];
+      const uint32_t tg = e >> 16;
+      vi = (tg == static_cast<uint32_t>(i)) ? (e & 0xffffu) : vi;
+      vj = (tg == j) ? (e & 0xffffu) : vj;
+    }
+    const uint32_t sel = (j == static_cast<uint32_t>(i)) ? vi : vj;
+    map[i * ms] = (j << 16) | vi;
+    BMc[(sel >> 5) * T] |= 1u << (sel & 31);
+    smin = min(smin, sel);
+  }
+  return smin;
+}
+
 // Saturated binomial C(a, b) from the exact pair's table, indexed by
 // (a, min(b, a-b)); callers guarantee a - b <= n - k and b <= k.
 __device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int stride, int a, int b) {

@@ -33,29 +33,36 @@ __device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
   return r;
 }
 
+// Shared-memory event cells are u16 pairs packed in u32 words (a block
+// handles at most 4096 scenarios, so a cell never exceeds 4096); global
+// cells are u32.
 template <bool SMEM_EVT>
-__device__ __forceinline__ void evt_add(uint32_t* a) {
+__device__ __forceinline__ void evt_add(uint32_t* base, int idx) {
   if (SMEM_EVT) {
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(a)))
-                 : "memory");
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(base + (idx >> 1)));
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(1u << ((idx & 1) << 4)) : "memory");
   } else {
-    atomicAdd(a, 1u);
+    atomicAdd(base + idx, 1u);
   }
 }
 
 // Walk the rows of one depth.  BMc: this thread's bitmap column (stride T),
-// with at least one zero word past the last slot word.
+// with at least one zero word past the last slot word.  Planes hold the
+// distance to the running maximum, dist = mx - count, in B bits per stage:
+//   hit     = R & (dist == 0)            OR-reduce of the planes
+//   on hit  : mx++ ; dist += 1 (all)     (rare: at most tmax times)
+//   always  : dist -= R                  (borrow chain, 2B ops per word)
 template <int W, int B, bool SMEM_EVT>
 __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P, int Dm,
-                                          uint32_t* eb) {
-  uint32_t C[B][W];
+                                          uint32_t* eb, int eoff) {
+  uint32_t Dp[B][W];
 #pragma unroll
   for (int l = 0; l < B; ++l)
 #pragma unroll
-    for (int w = 0; w < W; ++w) C[l][w] = 0u;
+    for (int w = 0; w < W; ++w) Dp[l][w] = 0u;
   const uint32_t tail = P - 32u * (W - 1);  // bits in the last word (1..32)
   const uint32_t tmask = tail >= 32u ? 0xffffffffu : ((1u << tail) - 1u);
-  uint32_t mx = 0;
+  int mx = 0;
   uint32_t pos = 0;
   for (int x = 0; x < Dm; ++x, pos += P) {
     const uint32_t wi = pos >> 5, sh = pos & 31u;
@@ -68,30 +75,32 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
       lo = hi;
     }
     R[W - 1] &= tmask;
-    // positions at count == mx that this row hits
     uint32_t hit = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      uint32_t eq = R[w];
+      uint32_t z = 0;
 #pragma unroll
-      for (int l = 0; l < B; ++l) {
-        const uint32_t m = ((mx >> l) & 1u) ? 0u : 0xffffffffu;  // select C or ~C
-        eq &= C[l][w] ^ m;
-      }
-      hit |= eq;
+      for (int l = 0; l < B; ++l) z |= Dp[l][w];
+      hit |= R[w] & ~z;
     }
-    if (hit) {
+    // dist' = dist + inc - R with inc = (hit != 0): where R = 1 and inc = 1
+    // nothing changes, so the update is one chain of +1 (inc) or -1 (!inc)
+    // over the mask c = inc ? ~R : R — branch-free, no divergence on events.
+    const bool inc = hit != 0;
+    if (inc) {
       ++mx;
-      if (mx >= 2u) evt_add<SMEM_EVT>(eb + (static_cast<int>(mx) - 2) * Dm + x);
+      if (mx >= 2) evt_add<SMEM_EVT>(eb, eoff + (mx - 2) * Dm + x);
     }
+    const uint32_t flip = inc ? 0u : 0xffffffffu;  // borrow uses ~dist
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      uint32_t carry = R[w];
+      uint32_t c = inc ? ~R[w] : R[w];
+      if (w == W - 1) c &= tmask;
 #pragma unroll
       for (int l = 0; l < B; ++l) {
-        const uint32_t t = C[l][w] & carry;
-        C[l][w] ^= carry;
-        carry = t;
+        const uint32_t t = (Dp[l][w] ^ flip) & c;
+        Dp[l][w] ^= c;
+        c = t;
       }
     }
   }
@@ -99,21 +108,23 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
 
 template <int W, bool SMEM_EVT>
 __device__ __forceinline__ void walk_rows_b(int b, const uint32_t* BMc, int T, uint32_t P, int Dm,
-                                            uint32_t* eb) {
+                                            uint32_t* eb, int eoff) {
   switch (b) {
-    case 2: walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    case 3: walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    case 4: walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    case 5: walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    case 6: walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    case 7: walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb); break;
-    default: walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb); break;
+    case 2: walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    case 3: walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    case 4: walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    case 5: walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    case 6: walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    case 7: walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+    default: walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
   }
 }
 
 }  // namespace
 
-template <int KREG, bool SMEM_EVT>
+// KREG > 0: register-resident Fisher-Yates map for k <= KREG; 0: shared-memory
+// map (any k).  WMAX: largest ceil(P/32) among the work item's depths.
+template <int KREG, int WMAX, bool SMEM_EVT>
 __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __restrict__ work,
                                                            const PairDesc* __restrict__ pairs,
                                                            const EntryDesc* __restrict__ entries,
@@ -130,43 +141,35 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   const int k = pd.k, n = pd.n;
   const int nw = (n + 31) >> 5;
   const bool own_h0 = (w.e_lo == pd.entry_base);
+  const int evt_words = SMEM_EVT ? (w.evt_len + 1) / 2 : 0;
 
   unsigned char* p = smem;
   EntryDesc* ents = carve<EntryDesc>(p, ne > 0 ? ne : 1);
   DrawConst* dc = carve<DrawConst>(p, k > 0 ? k : 1);
   uint32_t* h0 = carve<uint32_t>(p, n);
-  uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, w.evt_len) : nullptr;
+  uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, evt_words) : nullptr;
   uint32_t* BM = carve<uint32_t>(p, static_cast<size_t>(nw + 1) * T);  // +1 zero word
   uint32_t* MAP = (KREG == 0) ? carve<uint32_t>(p, static_cast<size_t>(k > 0 ? k : 1) * T) : nullptr;
-  uint16_t* SS = (KREG == 0) ? carve<uint16_t>(p, static_cast<size_t>(k > 0 ? k : 1) * T) : nullptr;
 
   for (int i = tid; i < ne; i += T) {
     EntryDesc e = entries[w.e_lo + i];
-    if (SMEM_EVT) e.evt_off -= w.evt_lo;
+    e.evt_off -= w.evt_lo;  // cell index relative to the work item's range
     ents[i] = e;
   }
   if (!pd.exact)
     for (int i = tid; i < k; i += T) dc[i] = draws[pd.draw_off + i];
   for (int i = tid; i < n; i += T) h0[i] = 0u;
-  if (SMEM_EVT)
-    for (int i = tid; i < w.evt_len; i += T) evt[i] = 0u;
+  for (int i = tid; i < evt_words; i += T) evt[i] = 0u;
   __syncthreads();
-  uint32_t* evt_base = SMEM_EVT ? evt : evt_g;
+  uint32_t* evt_base = SMEM_EVT ? evt : evt_g + w.evt_lo;
   uint32_t* BMc = BM + tid;
 
   for (uint64_t t = w.t0 + tid; t < w.t1; t += T) {
     uint32_t s0 = 0;
+    for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
     if (KREG > 0 && !pd.exact) {
-      uint32_t s[KREG > 0 ? KREG : 1];
-      gen_mc_regs<(KREG > 0 ? KREG : 1)>(pd.seed, t, k, dc, s);
-      for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
-#pragma unroll
-      for (int j = 0; j < (KREG > 0 ? KREG : 1); ++j)
-        if (j < k) BMc[(s[j] >> 5) * T] |= 1u << (s[j] & 31);
-      s0 = s[0];
+      s0 = gen_mc_bitmap<(KREG > 0 ? KREG : 1)>(pd.seed, t, k, dc, BMc, T);
     } else if (pd.exact) {
-      // unrank into the bitmap directly
-      for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
       uint64_t rank = t;
       int c = 0;
       for (int i = 0; i < k; ++i) {
@@ -182,9 +185,7 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
         ++c;
       }
     } else {
-      gen_mc_generic(pd.seed, t, n, k, dc, MAP + tid, T, BMc, T, SS + tid, T);
-      BMc[nw * T] = 0u;
-      s0 = SS[tid];
+      s0 = gen_mc_bitmap_smem(pd.seed, t, k, dc, MAP + tid, T, BMc, T);
     }
     if (own_h0 && k > 0) atomicAdd(&h0[s0], 1u);
 
@@ -193,16 +194,22 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
       const uint32_t P = static_cast<uint32_t>(e.P);
       const int Dm = e.Dmax;
       const int b = 32 - __clz(static_cast<uint32_t>(e.tmax));  // bits of tmax (>= 2)
-      uint32_t* eb = evt_base + e.evt_off;
+      const int eo = e.evt_off;
       switch ((P + 31u) >> 5) {
-        case 1: walk_rows_b<1, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 2: walk_rows_b<2, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 3: walk_rows_b<3, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 4: walk_rows_b<4, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 5: walk_rows_b<5, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 6: walk_rows_b<6, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        case 7: walk_rows_b<7, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
-        default: walk_rows_b<8, SMEM_EVT>(b, BMc, T, P, Dm, eb); break;
+        case 1: walk_rows_b<1, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+        case 2: walk_rows_b<2, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+        case 3: walk_rows_b<3, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+        case 4: walk_rows_b<4, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+        default:
+          if (WMAX > 4) {
+            switch ((P + 31u) >> 5) {
+              case 5: walk_rows_b<5, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+              case 6: walk_rows_b<6, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+              case 7: walk_rows_b<7, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+              default: walk_rows_b<8, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+            }
+          }
+          break;
       }
     }
   }
@@ -210,17 +217,19 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   if (own_h0)
     for (int i = tid; i < n; i += T)
       if (h0[i]) atomicAdd(&h0_g[pd.h0_off + i], h0[i]);
-  if (SMEM_EVT)
-    for (int i = tid; i < w.evt_len; i += T)
-      if (evt[i]) atomicAdd(&evt_g[w.evt_lo + i], evt[i]);
+  for (int i = tid; i < evt_words; i += T) {
+    const uint32_t v = evt[i];
+    if (v & 0xffffu) atomicAdd(&evt_g[w.evt_lo + 2 * i], v & 0xffffu);
+    if (v >> 16) atomicAdd(&evt_g[w.evt_lo + 2 * i + 1], v >> 16);
+  }
 }
 
-template <int KREG, bool SM>
+template <int KREG, int WMAX, bool SM>
 static cudaError_t launch_rows_t(int blocks, int threads, size_t smem, cudaStream_t st,
                                  const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
                                  const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
                                  uint32_t* h0) {
-  auto fn = hist_rows_kernel<KREG, SM>;
+  auto fn = hist_rows_kernel<KREG, WMAX, SM>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -228,19 +237,22 @@ static cudaError_t launch_rows_t(int blocks, int threads, size_t smem, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t launch_hist_rows(int kreg, bool smem_evt, int blocks, int threads, size_t smem,
-                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
-                             const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
-                             uint32_t* evt, uint32_t* h0) {
+// kreg in {0, 16, 32, 64}; wmax in {4, 8}
+cudaError_t launch_hist_rows(int kreg, int wmax, bool smem_evt, int blocks, int threads,
+                             size_t smem, cudaStream_t st, const WorkItem* w,
+                             const PairDesc* pairs, const EntryDesc* ents, const DrawConst* dr,
+                             const uint64_t* binom, uint32_t* evt, uint32_t* h0) {
   if (blocks <= 0) return cudaSuccess;
-#define LP_W(K)                                                                                   \
-  if (kreg == K)                                                                                  \
-    return smem_evt ? launch_rows_t<K, true>(blocks, threads, smem, st, w, pairs, ents, dr, binom, \
-                                             evt, h0)                                             \
-                    : launch_rows_t<K, false>(blocks, threads, smem, st, w, pairs, ents, dr,      \
-                                              binom, evt, h0);
-  LP_W(0)
-  LP_W(16)
+#define LP_W(K, WM)                                                                              \
+  if (kreg == K && wmax == WM)                                                                   \
+    return smem_evt ? launch_rows_t<K, WM, true>(blocks, threads, smem, st, w, pairs, ents, dr,  \
+                                                 binom, evt, h0)                                 \
+                    : launch_rows_t<K, WM, false>(blocks, threads, smem, st, w, pairs, ents, dr, \
+                                                  binom, evt, h0);
+  LP_W(0, 4)
+  LP_W(0, 8)
+  LP_W(16, 4)
+  LP_W(16, 8)
 #undef LP_W
   return cudaErrorInvalidValue;
 }
