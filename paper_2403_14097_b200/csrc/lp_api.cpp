@@ -655,6 +655,7 @@ struct lp_handle {
   size_t off_divtab = 0;
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
+  size_t w_histp = 0;
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
          w_plan = 0, w_live = 0, w_final = 0;
   DevBuf tables, work;
@@ -1080,6 +1081,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
   h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
   h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
+  h->w_histp = take(8 * std::max<int64_t>(h->hp.hist_len, 1));
   h->w_val = take(8 * nn);
   h->w_mig = take(8 * nn);
   h->w_par = take(4 * nn);
@@ -1139,10 +1141,13 @@ lp_status lp_execute(lp_handle* h) {
   int32_t* par = dptr<int32_t>(h->work, h->w_par);
   double* stc = dptr<double>(h->work, h->w_stc);
   double* stm = dptr<double>(h->work, h->w_stm);
+  double* histp = dptr<double>(h->work, h->w_histp);
+  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist, histp));
+  ++launches;
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
   for (int j = 0; j < h->horizon; ++j) {
-    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, pcost, d.hist, thr, throw_,
+    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, pcost, histp, thr, throw_,
                               h->S, val, mig, par, stc, stm));
     ++launches;
   }

@@ -62,10 +62,12 @@ __device__ __forceinline__ double transition_cost(int m, int sd, int sp, int td,
 }
 
 // phi(prev, next, n_now, n_next) from the prev config's deficit histogram
-// (rows d = 0..min(k, D), m = D - d).  thr_tab/thr_row: throughput(D, P).
+// (rows d = 0..min(k, D), m = D - d).  prob(d) returns hist[m] of the
+// reference, count_m / count (0.0 for an empty bin).  thr_tab/thr_row:
+// throughput(D, P).
+template <class Prob>
 __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
-                                          const LevelDesc& L, const DpScalars& S,
-                                          const uint32_t* __restrict__ hist,
+                                          const LevelDesc& L, const DpScalars& S, Prob prob,
                                           const double* __restrict__ thr_tab,
                                           const int32_t* __restrict__ thr_row) {
   PhiOut o{0.0, 0.0};
@@ -76,15 +78,12 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     o.committed = __dmul_rn(nc.thr, (0.0 < te) ? te : 0.0);
     return o;
   }
-  const uint32_t* h = hist + pv.hist_off;
-  const double total = static_cast<double>(L.total);
   const int dmax = min(L.k, pv.d);
   double committed = 0.0, cost_sum = 0.0;
   for (int d = dmax; d >= 0; --d) {  // m = D - d ascending
-    const uint32_t cnt = h[d];
-    if (cnt == 0u) continue;
+    const double p = prob(d);
+    if (p == 0.0) continue;
     const int m = pv.d - d;
-    const double p = __ddiv_rn(static_cast<double>(cnt), total);
     bool rb;
     double cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
     if (rb) cost = __dadd_rn(cost, S.rollback);
@@ -101,6 +100,21 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
   o.committed = committed;
   o.mig = cost_sum;
   return o;
+}
+
+// hist[m] = count_m / count, once per re-plan (after the cross-rank reduce),
+// so the DP's inner loop has no FP64 division.  One block per depth entry.
+__global__ void normalize_kernel(const PairDesc* __restrict__ pairs,
+                                 const EntryDesc* __restrict__ entries,
+                                 const uint32_t* __restrict__ hist, double* __restrict__ histp) {
+  const EntryDesc e = entries[blockIdx.x];
+  const PairDesc pd = pairs[e.pair];
+  const int len = hist_row(e.Dmax + 1, pd.k);
+  const double total = static_cast<double>(pd.count);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const uint32_t c = hist[e.hist_off + i];
+    histp[e.hist_off + i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
+  }
 }
 
 struct Cand {
@@ -136,7 +150,7 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 __global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
                                                       const NodeCfg* __restrict__ cfg,
                                                       const double4* __restrict__ pcost,
-                                                      const uint32_t* __restrict__ hist,
+                                                      const double* __restrict__ histp,
                                                       const double* __restrict__ thr_tab,
                                                       const int32_t* __restrict__ thr_row,
                                                       DpScalars S, double* __restrict__ val,
@@ -162,7 +176,8 @@ __global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __
   for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
     const int gi = L.prev_base + pi;
     const NodeCfg pv = cfg[gi];
-    const PhiOut ph = phi_dev(pv, nx, nc, L, S, hist, thr_tab, thr_row);
+    const double* hp = histp + pv.hist_off;
+    const PhiOut ph = phi_dev(pv, nx, nc, L, S, [hp](int d) { return hp[d]; }, thr_tab, thr_row);
     const double v = __dadd_rn(val[gi], ph.committed);
     const double mg = __dadd_rn(mig[gi], ph.mig);
     if (best.idx < 0 || v > best.value || (v == best.value && mg < best.mig)) {
@@ -289,20 +304,32 @@ __global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc
                                   const uint32_t* __restrict__ hist,
                                   const double* __restrict__ thr_tab,
                                   const int32_t* __restrict__ thr_row, double* __restrict__ out2) {
-  const PhiOut o = phi_dev(pv, nx, nc, L, S, hist, thr_tab, thr_row);
+  const double total = static_cast<double>(L.total);
+  const uint32_t* h = hist + pv.hist_off;
+  const PhiOut o = phi_dev(
+      pv, nx, nc, L, S,
+      [h, total](int d) { return h[d] ? __ddiv_rn(static_cast<double>(h[d]), total) : 0.0; },
+      thr_tab, thr_row);
   out2[0] = o.committed;
   out2[1] = o.mig;
 }
 
 // ---------------------------------------------------------------------------
 cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
-                           const NodeCfg* cfg, const double4* pcost, const uint32_t* hist,
+                           const NodeCfg* cfg, const double4* pcost, const double* histp,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm) {
   const int blocks = next_count;
   if (blocks <= 0) return cudaSuccess;
-  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, pcost, hist, thr_tab, thr_row, S, val,
+  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val,
                                              mig, parent, stc, stm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
+                             const EntryDesc* ents, const uint32_t* hist, double* histp) {
+  if (n_entries <= 0) return cudaSuccess;
+  normalize_kernel<<<n_entries, 128, 0, st>>>(pairs, ents, hist, histp);
   return cudaGetLastError();
 }
 

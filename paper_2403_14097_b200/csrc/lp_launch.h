@@ -36,9 +36,11 @@ cudaError_t launch_dump(int n, int k, int exact, int trials, uint64_t seed, cons
                         cudaStream_t st);
 
 cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
-                           const NodeCfg* cfg, const double4* pcost, const uint32_t* hist,
+                           const NodeCfg* cfg, const double4* pcost, const double* histp,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm);
+cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
+                             const EntryDesc* ents, const uint32_t* hist, double* histp);
 cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
                             const NodeCfg* cfg, const double* val, const double* mig,
                             const int32_t* parent, const double* stc, const double* stm,
