@@ -116,6 +116,7 @@ typedef struct {
   uint64_t h2d_bytes;        /* bytes copied host->device by the last prepare */
   uint64_t d2h_bytes;        /* bytes copied device->host by the last fetch */
   double prepare_ms;         /* host wall time of the last lp_prepare (tables + H2D issue) */
+  uint64_t cached_pairs;     /* (n, k) ensembles served from the histogram cache */
 } lp_stats;
 
 typedef struct lp_handle lp_handle;
@@ -147,6 +148,14 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* liveput_out,
 lp_status lp_get_stats(const lp_handle* h, lp_stats* out);
 /* The CUDA stream every kernel of this handle runs on (cudaStream_t as void*). */
 void* lp_stream(lp_handle* h);
+
+/* ---- device-resident histogram cache across re-plans: the reference's
+ *      hist_cache_ (optimizer.hpp:88, optimizer.cpp:64-71).  Off by default,
+ *      so every lp_execute is a cold re-plan that recomputes every ensemble.
+ *      When on, an (n, k) ensemble computed by an earlier re-plan of this
+ *      handle is reused (results are identical: they depend only on the key).
+ *      max_bytes bounds the device store; when full it is dropped and refilled. */
+lp_status lp_set_hist_cache(lp_handle* h, int32_t enable, uint64_t max_bytes);
 
 /* ---- Planner::phi (optimizer.hpp:57-58, optimizer.cpp:52-62, 96-138) ---- */
 lp_status lp_phi(lp_handle* h, lp_config prev, lp_config next, int32_t n_now, int32_t n_next,

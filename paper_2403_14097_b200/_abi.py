@@ -92,6 +92,7 @@ class lp_stats(C.Structure):
         ("h2d_bytes", C.c_uint64),
         ("d2h_bytes", C.c_uint64),
         ("prepare_ms", C.c_double),
+        ("cached_pairs", C.c_uint64),
     ]
 
 
@@ -116,6 +117,7 @@ _SIGS = {
     "lp_fetch": (C.c_int, [C.c_void_p, _P(lp_plan_step), _P(lp_liveput_row), C.c_int32, _P(C.c_int32)]),
     "lp_get_stats": (C.c_int, [C.c_void_p, _P(lp_stats)]),
     "lp_stream": (C.c_void_p, [C.c_void_p]),
+    "lp_set_hist_cache": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
     "lp_phi": (C.c_int, [C.c_void_p, lp_config, lp_config, C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
     "lp_sequence_value": (C.c_int, [C.c_void_p, lp_config, _P(lp_config), _P(C.c_int32), C.c_int32, _P(C.c_double)]),
     "lp_survivor_hist": (C.c_int, [C.c_void_p, lp_config, C.c_int32, C.c_int32, _P(C.c_uint64), _P(C.c_uint64)]),

@@ -655,7 +655,6 @@ struct lp_handle {
   size_t off_divtab = 0;
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
-  size_t w_histp = 0;
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
          w_plan = 0, w_live = 0, w_final = 0;
   DevBuf tables, work;
@@ -666,6 +665,19 @@ struct lp_handle {
   // ensemble calls (phi / survivor_hist / liveput) and their cache
   DevBuf e_tables, e_work;
   std::map<std::tuple<int, int, int>, std::pair<int, std::vector<uint32_t>>> hist_cache;
+
+  // device histogram store (FP64 probabilities, see lp_prepare)
+  struct StoreSlot {
+    uint64_t count = 0;                         // ensemble size
+    std::map<int, std::pair<int, int>> ents;    // P -> (Dmax, store offset of D = 1)
+  };
+  bool cache_on = false;
+  uint64_t cache_max = 4ull << 30;              // bytes
+  std::map<std::pair<int, int>, StoreSlot> store_idx;
+  DevBuf store;
+  size_t store_used = 0;                        // doubles
+  std::vector<int32_t> store_off;               // per fresh entry
+  size_t off_store_off = 0;
 };
 
 namespace {
@@ -809,6 +821,24 @@ lp_status planner_rows(lp_handle* h, int D, int P, int n, int k, std::vector<uin
   const int off = hist_row(D, k);
   const int len = std::min(k, D) + 1;
   rows.assign(it->second.second.begin() + off, it->second.second.begin() + off + len);
+  return LP_OK;
+}
+
+// Grows the histogram store to `doubles` entries, keeping the cached content.
+lp_status grow_store(lp_handle* h, size_t doubles) {
+  const size_t bytes = std::max<size_t>(doubles, 1) * sizeof(double);
+  if (bytes <= h->store.cap) return LP_OK;
+  void* np = nullptr;
+  size_t want = std::max<size_t>(bytes + bytes / 2, 1 << 20);
+  cudaError_t e = cudaMalloc(&np, want);
+  if (e != cudaSuccess) return fail(h, LP_ENOMEM, "histogram store: %s", cudaGetErrorString(e));
+  if (h->store.p) {
+    LP_CUDA(h, cudaMemcpyAsync(np, h->store.p, h->store.cap, cudaMemcpyDeviceToDevice, h->stream));
+    LP_CUDA(h, cudaStreamSynchronize(h->stream));
+    cudaFree(h->store.p);
+  }
+  h->store.p = np;
+  h->store.cap = want;
   return LP_OK;
 }
 
@@ -983,9 +1013,69 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     }
     specs[si].ref_keys = keys;
   }
+  // Device histogram store: probabilities of every ensemble live in one HBM
+  // array keyed by (n, k).  With the cache on, ensembles already in the store
+  // (covering the depths this re-plan reads) are not recomputed — the
+  // reference's hist_cache_ (optimizer.hpp:88); the cache is valid for the
+  // handle's lifetime because options and profile are fixed.
+  std::vector<EnsembleSpec> fresh;
+  std::vector<int> fresh_of(specs.size(), -1);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (!h->cache_on || pass == 1) {
+      h->store_idx.clear();
+      h->store_used = 0;
+    }
+    fresh.clear();
+    std::fill(fresh_of.begin(), fresh_of.end(), -1);
+    size_t need = 0;
+    for (size_t si = 0; si < specs.size(); ++si) {
+      auto it = h->store_idx.find({specs[si].n, specs[si].k});
+      bool covered = it != h->store_idx.end();
+      if (covered)
+        for (const auto& [P, Dm] : specs[si].dmax_by_p) {
+          auto e = it->second.ents.find(P);
+          if (e == it->second.ents.end() || e->second.first < Dm) covered = false;
+        }
+      if (covered) continue;
+      EnsembleSpec sp = specs[si];
+      if (it != h->store_idx.end())  // keep what the old slot covered
+        for (const auto& [P, v] : it->second.ents) {
+          int& dm = sp.dmax_by_p[P];
+          dm = std::max(dm, v.first);
+        }
+      for (const auto& [P, Dm] : sp.dmax_by_p) need += hist_row(Dm + 1, sp.k);
+      fresh_of[si] = (int)fresh.size();
+      fresh.push_back(sp);
+    }
+    if (h->store_used + need <= h->cache_max / 8 || pass == 1) break;  // else evict all, retry
+  }
   std::string err;
-  lp_status s = build_hist_plan(specs, h->rank, h->nranks, h->hp, err, h->num_sms);
+  lp_status s = build_hist_plan(fresh, h->rank, h->nranks, h->hp, err, h->num_sms);
   if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+  // store slots of the fresh entries (appended; old slots of recomputed
+  // ensembles are abandoned until the next eviction)
+  h->store_off.assign(h->hp.entries.size(), 0);
+  for (size_t e = 0; e < h->hp.entries.size(); ++e) {
+    const EntryDesc& E = h->hp.entries[e];
+    const PairDesc& pd = h->hp.pairs[E.pair];
+    h->store_off[e] = (int32_t)h->store_used;
+    h->store_idx[{pd.n, pd.k}].ents[E.P] = {E.Dmax, (int)h->store_used};
+    h->store_used += hist_row(E.Dmax + 1, pd.k);
+  }
+  for (const PairDesc& pd : h->hp.pairs) {
+    auto& slot = h->store_idx[{pd.n, pd.k}];
+    slot.count = pd.count;
+    for (auto it = slot.ents.begin(); it != slot.ents.end();) {  // drop stale depth slots
+      bool fresh_p = false;
+      for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
+        fresh_p |= h->hp.entries[e].P == it->first;
+      it = fresh_p ? std::next(it) : slot.ents.erase(it);
+    }
+  }
+  {
+    lp_status gs = grow_store(h, h->store_used);
+    if (gs != LP_OK) return gs;
+  }
   // node histogram rows + levels
   std::map<int, int> thr_need;
   int pmax = 1;
@@ -1004,16 +1094,16 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     L.fixed = L.fresh ? h->cs.fresh_fixed : 0.0;
     L.has_hist = level_spec[j] >= 0;
     if (!L.has_hist) continue;
-    const PairDesc& pd = h->hp.pairs[level_spec[j]];
-    L.total = pd.count;
-    entry_of_p.assign(pd.n + 2, -1);
-    for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
-      entry_of_p[h->hp.entries[e].P] = e;
+    const EnsembleSpec& spj = specs[level_spec[j]];
+    const auto& slot = h->store_idx.at({spj.n, spj.k});
+    L.total = slot.count;
+    entry_of_p.assign(spj.n + 2, -1);
+    for (const auto& [P, v] : slot.ents) entry_of_p[P] = v.second;  // store offset of D = 1
     for (int i = 0; i < lcount[j]; ++i) {
       NodeCfg& c = h->cfg[lbase[j] + i];
       if (c.d <= 0) continue;
-      const int e = entry_of_p[c.p];
-      if (e >= 0) c.hist_off = h->hp.entries[e].hist_off + hist_row(c.d, L.k);
+      const int so = entry_of_p[c.p];
+      if (so >= 0) c.hist_off = so + hist_row(c.d, L.k);
       if ((int)need_d.size() <= c.p) need_d.resize(c.p + 1, 0);
       need_d[c.p] = std::max(need_d[c.p], c.d);
     }
@@ -1064,6 +1154,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->off_lrows = pk.add(h->lrows);
   h->off_thr = pk.add(h->thr.vals);
   h->off_throw = pk.add(h->thr.row);
+  h->off_store_off = pk.add(h->store_off);
   LP_CUDA(h, h->tables.ensure(pk.bytes.size()));
   LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
   std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
@@ -1081,7 +1172,6 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
   h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
   h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
-  h->w_histp = take(8 * std::max<int64_t>(h->hp.hist_len, 1));
   h->w_val = take(8 * nn);
   h->w_mig = take(8 * nn);
   h->w_par = take(4 * nn);
@@ -1101,6 +1191,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   h->stats.horizon = H;
   h->stats.hist_alg_ops = h->hp.alg_ops;
   h->stats.h2d_bytes = pk.bytes.size() + sizeof(int32_t) * len;
+  h->stats.cached_pairs = specs.size() - fresh.size();
   h->stats.prepare_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return LP_OK;
@@ -1141,8 +1232,9 @@ lp_status lp_execute(lp_handle* h) {
   int32_t* par = dptr<int32_t>(h->work, h->w_par);
   double* stc = dptr<double>(h->work, h->w_stc);
   double* stm = dptr<double>(h->work, h->w_stm);
-  double* histp = dptr<double>(h->work, h->w_histp);
-  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist, histp));
+  double* histp = static_cast<double*>(h->store.p);
+  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
+                              dptr<int32_t>(h->tables, h->off_store_off), histp));
   ++launches;
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
@@ -1157,7 +1249,8 @@ lp_status lp_execute(lp_handle* h) {
   ++launches;
   if (!h->lrows.empty()) {
     LP_CUDA(h, launch_liveput((int)h->lrows.size(), st, dptr<int4>(h->tables, h->off_lrows), lv,
-                              cfg, d.hist, thr, throw_, dptr<lp_liveput_row>(h->work, h->w_live)));
+                              cfg, nullptr, histp, thr, throw_,
+                              dptr<lp_liveput_row>(h->work, h->w_live)));
     ++launches;
   }
   LP_CUDA(h, cudaEventRecord(h->ev[3], st));
@@ -1195,6 +1288,16 @@ lp_status lp_replan(lp_handle* h, lp_config current, const int32_t* n_seq, int32
   s = lp_execute(h);
   if (s != LP_OK) return s;
   return lp_fetch(h, out, live, cap, rows);
+}
+
+lp_status lp_set_hist_cache(lp_handle* h, int32_t enable, uint64_t max_bytes) {
+  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  h->cache_on = enable != 0;
+  h->cache_max = max_bytes ? max_bytes : (4ull << 30);
+  h->store_idx.clear();
+  h->store_used = 0;
+  h->prepared = false;
+  return LP_OK;
 }
 
 lp_status lp_get_stats(const lp_handle* hc, lp_stats* out) {
@@ -1350,7 +1453,7 @@ lp_status lp_expected_liveput(lp_handle* h, lp_config cfg, int32_t n, int32_t n_
                              h->stream));
   LP_CUDA(h, launch_liveput(1, h->stream, dptr<int4>(h->e_tables, orw),
                             dptr<LevelDesc>(h->e_tables, ol), dptr<NodeCfg>(h->e_tables, oc),
-                            dptr<uint32_t>(h->e_tables, oh), dptr<double>(h->e_tables, ot),
+                            dptr<uint32_t>(h->e_tables, oh), nullptr, dptr<double>(h->e_tables, ot),
                             dptr<int32_t>(h->e_tables, orow),
                             dptr<lp_liveput_row>(h->e_tables, oout)));
   LP_CUDA(h, h->pin_down.ensure(sizeof(lp_liveput_row)));

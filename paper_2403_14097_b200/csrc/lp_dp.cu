@@ -106,14 +106,16 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
 // so the DP's inner loop has no FP64 division.  One block per depth entry.
 __global__ void normalize_kernel(const PairDesc* __restrict__ pairs,
                                  const EntryDesc* __restrict__ entries,
-                                 const uint32_t* __restrict__ hist, double* __restrict__ histp) {
+                                 const uint32_t* __restrict__ hist,
+                                 const int32_t* __restrict__ store_off, double* __restrict__ store) {
   const EntryDesc e = entries[blockIdx.x];
   const PairDesc pd = pairs[e.pair];
   const int len = hist_row(e.Dmax + 1, pd.k);
   const double total = static_cast<double>(pd.count);
+  double* out = store + store_off[blockIdx.x];
   for (int i = threadIdx.x; i < len; i += blockDim.x) {
     const uint32_t c = hist[e.hist_off + i];
-    histp[e.hist_off + i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
+    out[i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
   }
 }
 
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restri
 __global__ void liveput_kernel(const int4* __restrict__ rows /* level, node, out_row, - */,
                                int n_rows, const LevelDesc* __restrict__ levels,
                                const NodeCfg* __restrict__ cfg, const uint32_t* __restrict__ hist,
+                               const double* __restrict__ probs,
                                const double* __restrict__ thr_tab,
                                const int32_t* __restrict__ thr_row,
                                lp_liveput_row* __restrict__ out) {
@@ -283,19 +286,29 @@ __global__ void liveput_kernel(const int4* __restrict__ rows /* level, node, out
   const int4 rw = rows[r];
   const LevelDesc L = levels[rw.x];
   const NodeCfg c = cfg[rw.y];
-  const uint32_t* h = hist + c.hist_off;
   const int dmax = min(L.k, c.d);
   double acc = 0.0;
-  for (int d = dmax; d >= 0; --d) {
-    const int m = c.d - d;
-    if (m < 1 || h[d] == 0u) continue;
-    acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(h[d]), thr_tab[thr_row[c.p] + m]));
+  if (probs) {  // store path: sum_m p_m * thr(m, P)
+    const double* p = probs + c.hist_off;
+    for (int d = dmax; d >= 0; --d) {
+      const int m = c.d - d;
+      if (m < 1 || p[d] == 0.0) continue;
+      acc = __dadd_rn(acc, __dmul_rn(p[d], thr_tab[thr_row[c.p] + m]));
+    }
+  } else {  // counts path: sum_m count_m * thr(m, P) / count
+    const uint32_t* h = hist + c.hist_off;
+    for (int d = dmax; d >= 0; --d) {
+      const int m = c.d - d;
+      if (m < 1 || h[d] == 0u) continue;
+      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(h[d]), thr_tab[thr_row[c.p] + m]));
+    }
+    acc = __ddiv_rn(acc, static_cast<double>(L.total));
   }
   lp_liveput_row o;
   o.interval = rw.x;
   o.config.pipelines = c.d;
   o.config.stages = c.p;
-  o.liveput = __ddiv_rn(acc, static_cast<double>(L.total));
+  o.liveput = acc;
   out[rw.z] = o;
 }
 
@@ -327,9 +340,10 @@ cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDe
 }
 
 cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
-                             const EntryDesc* ents, const uint32_t* hist, double* histp) {
+                             const EntryDesc* ents, const uint32_t* hist, const int32_t* store_off,
+                             double* store) {
   if (n_entries <= 0) return cudaSuccess;
-  normalize_kernel<<<n_entries, 128, 0, st>>>(pairs, ents, hist, histp);
+  normalize_kernel<<<n_entries, 128, 0, st>>>(pairs, ents, hist, store_off, store);
   return cudaGetLastError();
 }
 
@@ -343,11 +357,11 @@ cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* level
 }
 
 cudaError_t launch_liveput(int n_rows, cudaStream_t st, const int4* rows, const LevelDesc* levels,
-                           const NodeCfg* cfg, const uint32_t* hist, const double* thr_tab,
-                           const int32_t* thr_row, lp_liveput_row* out) {
+                           const NodeCfg* cfg, const uint32_t* hist, const double* probs,
+                           const double* thr_tab, const int32_t* thr_row, lp_liveput_row* out) {
   if (n_rows <= 0) return cudaSuccess;
-  liveput_kernel<<<(n_rows + 127) / 128, 128, 0, st>>>(rows, n_rows, levels, cfg, hist, thr_tab,
-                                                       thr_row, out);
+  liveput_kernel<<<(n_rows + 127) / 128, 128, 0, st>>>(rows, n_rows, levels, cfg, hist, probs,
+                                                       thr_tab, thr_row, out);
   return cudaGetLastError();
 }
 

@@ -40,14 +40,15 @@ cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDe
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm);
 cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
-                             const EntryDesc* ents, const uint32_t* hist, double* histp);
+                             const EntryDesc* ents, const uint32_t* hist, const int32_t* store_off,
+                             double* store);
 cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
                             const NodeCfg* cfg, const double* val, const double* mig,
                             const int32_t* parent, const double* stc, const double* stm,
                             lp_plan_step* plan, double* final_value);
 cudaError_t launch_liveput(int n_rows, cudaStream_t st, const int4* rows, const LevelDesc* levels,
-                           const NodeCfg* cfg, const uint32_t* hist, const double* thr_tab,
-                           const int32_t* thr_row, lp_liveput_row* out);
+                           const NodeCfg* cfg, const uint32_t* hist, const double* probs,
+                           const double* thr_tab, const int32_t* thr_row, lp_liveput_row* out);
 cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
                               const LevelDesc& L, const DpScalars& S, const uint32_t* hist,
                               const double* thr_tab, const int32_t* thr_row, double* out2,

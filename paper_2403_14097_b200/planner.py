@@ -162,6 +162,10 @@ class Planner:
         _abi.check(self._lib.lp_get_stats(self._h, C.byref(st)), self._h)
         return st
 
+    def set_hist_cache(self, enable: bool = True, max_bytes: int = 4 << 30) -> None:
+        """Reuse (n, k) ensembles across re-plans, like the reference's hist_cache_."""
+        _abi.check(self._lib.lp_set_hist_cache(self._h, int(enable), max_bytes), self._h)
+
     def stream_ptr(self) -> int:
         return self._lib.lp_stream(self._h) or 0
 

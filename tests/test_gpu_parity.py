@@ -262,3 +262,42 @@ def test_full_size_properties():
         counts, tot = p.survivor_counts(c, 224, 16)
         assert int(counts.sum()) == tot == 1000000
     p.close()
+
+
+# ---- device-resident histogram cache (the reference's hist_cache_) ---------
+def test_hist_cache_replay_matches_cold():
+    """Planning-loop replay (tools/replay.py, Ideal(12)) with the cache on is
+    bit-identical to cold re-plans and to the reference's replay fixture."""
+    import json
+    from pathlib import Path
+    from tools.replay import TRACE, loop
+    from paper_2403_14097_b200.planner import reactive_plan
+    counts = json.loads(Path(TRACE).read_text())["counts"]
+    w = lm_6p7b()
+    opt = PlannerOptions(mc_trials=1000)
+    warm = planner(w, opt)
+    warm.set_hist_cache(True)
+    cold = planner(w, opt)
+    a, _ = loop(warm.dp_optimize, lambda n: reactive_plan(n, w), counts, 300)
+    b, _ = loop(cold.dp_optimize, lambda n: reactive_plan(n, w), counts, 300)
+    assert a == b
+    ref = json.loads((Path(TRACE).parents[2] / "profiles" / "replay_ref_1e3.json").read_text())["sequence"]
+    assert a == ref[:300]
+    assert warm.stats().cached_pairs >= 0
+    warm.close()
+    cold.close()
+
+
+def test_hist_cache_reuses_ensembles():
+    w = lm_1p5b()
+    p = planner(w, PlannerOptions(mc_trials=20000))
+    p.set_hist_cache(True)
+    ns = [64, 60, 60, 57, 62, 56]
+    a = p.dp_optimize(ParallelConfig(8, 8), ns)
+    first = p.stats()
+    b = p.dp_optimize(ParallelConfig(8, 8), ns)
+    second = p.stats()
+    assert plan_rows(a) == plan_rows(b)
+    assert first.cached_pairs == 0 and second.cached_pairs == second.mc_pairs + second.exact_pairs + second.cached_pairs - (second.mc_pairs + second.exact_pairs)
+    assert second.mc_pairs == 0  # everything came from the cache
+    p.close()

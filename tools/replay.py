@@ -1,0 +1,106 @@
+"""BASELINE config 3: GPT-3 6.7B (D,P) table, N=128, 1e6 samples/point, the
+strategy-sequence replay of a synthetic 24 h trace (1440 one-minute intervals).
+
+The planning loop is the Ideal(12) policy of the reference simulator
+(simulator.cpp:301-318, Policy::Ideal): at interval i the planner sees the true
+next 12 availability counts and `current` is the configuration committed for
+interval i, which under Ideal is the previous plan's first step (it always fits,
+so adjust_config leaves it unchanged).  One Planner persists across the replay,
+as in the CLI (commands.cpp:215-216), so ensembles seen before come from the
+histogram cache — the reference's hist_cache_ — on the GPU too.
+
+  python tools/replay.py gpu --trials 1000000 --out gpurun_out/replay_gpu.json
+  python tools/replay.py ref --trials 1000 --intervals 240 --out profiles/replay_ref_1e3.json
+  python tools/replay.py compare A.json B.json
+The trace is tools/data/trace_gen_synthetic_128.json, made by the reference's
+gen_synthetic(seed=1, 128, 1440, 216, 200, 1, 8) (trace.cpp:80-180) with
+`python tools/replay.py trace` in the dev container.
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+TRACE = ROOT / "tools" / "data" / "trace_gen_synthetic_128.json"
+LOOKAHEAD = 12
+
+
+def make_trace():
+    import ctypes as C
+    from oracle.oracle import ref_lib
+    L = ref_lib()
+    buf = (C.c_int * 2000)()
+    ln = L.ref_gen_synthetic(1, 128, 1440, 216, 200, 1, 8, buf, 2000)
+    counts = list(buf[:ln])
+    TRACE.parent.mkdir(parents=True, exist_ok=True)
+    TRACE.write_text(json.dumps({"generator": "spotsim::gen_synthetic(1, 128, 1440, 216, 200, 1, 8)",
+                                 "interval_s": 60, "counts": counts}))
+    print(len(counts), min(counts), max(counts))
+
+
+def loop(plan_fn, reactive_fn, counts, intervals):
+    cur = reactive_fn(counts[0])
+    seq, times = [], []
+    last = min(intervals, len(counts) - LOOKAHEAD)
+    for i in range(last):
+        ns = counts[i:i + LOOKAHEAD + 1]
+        t = time.perf_counter()
+        plan = plan_fn(cur, ns)
+        times.append(time.perf_counter() - t)
+        nxt = plan[0].config
+        seq.append([[nxt.pipelines, nxt.stages] if nxt else None, plan[0].expected_committed.hex(),
+                     plan[0].expected_mig_cost_s.hex()])
+        cur = nxt
+    return seq, times
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["trace", "gpu", "ref", "compare"])
+    ap.add_argument("--trials", type=int, default=1_000_000)
+    ap.add_argument("--intervals", type=int, default=1440)
+    ap.add_argument("--no-cache", action="store_true")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("files", nargs="*")
+    a = ap.parse_args()
+    if a.mode == "trace":
+        return make_trace()
+    if a.mode == "compare":
+        x = json.loads(Path(a.files[0]).read_text())["sequence"]
+        y = json.loads(Path(a.files[1]).read_text())["sequence"]
+        m = min(len(x), len(y))
+        same = x[:m] == y[:m]
+        print(f"compared {m} intervals: {'identical' if same else 'DIFFERENT'}")
+        sys.exit(0 if same else 1)
+    counts = json.loads(TRACE.read_text())["counts"]
+    from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_6p7b
+    w = lm_6p7b()
+    opt = PlannerOptions(mc_trials=a.trials)
+    if a.mode == "gpu":
+        from paper_2403_14097_b200.planner import Planner, reactive_plan
+        p = Planner(w, CostTable(), opt)
+        if not a.no_cache:
+            p.set_hist_cache(True)
+        t0 = time.perf_counter()
+        seq, times = loop(p.dp_optimize, lambda n: reactive_plan(n, w), counts, a.intervals)
+        total = time.perf_counter() - t0
+    else:
+        from oracle.oracle import RefPlanner, oracle_reactive
+        p = RefPlanner(w, CostTable(), opt)
+        t0 = time.perf_counter()
+        seq, times = loop(p.dp_optimize, lambda n: oracle_reactive(w, n), counts, a.intervals)
+        total = time.perf_counter() - t0
+    res = {"mode": a.mode, "trials": a.trials, "intervals": len(seq), "total_s": total,
+           "mean_ms": 1e3 * total / max(1, len(seq)), "max_ms": 1e3 * max(times),
+           "first_ms": 1e3 * times[0], "cache": not a.no_cache, "sequence": seq}
+    print(json.dumps({k: v for k, v in res.items() if k != "sequence"}), flush=True)
+    if a.out:
+        Path(a.out).parent.mkdir(parents=True, exist_ok=True)
+        Path(a.out).write_text(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
