@@ -298,6 +298,6 @@ def test_hist_cache_reuses_ensembles():
     b = p.dp_optimize(ParallelConfig(8, 8), ns)
     second = p.stats()
     assert plan_rows(a) == plan_rows(b)
-    assert first.cached_pairs == 0 and second.cached_pairs == second.mc_pairs + second.exact_pairs + second.cached_pairs - (second.mc_pairs + second.exact_pairs)
-    assert second.mc_pairs == 0  # everything came from the cache
+    assert first.cached_pairs == 0 and first.mc_pairs > 0
+    assert second.mc_pairs == 0 and second.cached_pairs > 0  # everything came from the cache
     p.close()
