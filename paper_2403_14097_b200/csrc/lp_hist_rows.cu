@@ -106,18 +106,80 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
   }
 }
 
-template <int W, bool SMEM_EVT>
-__device__ __forceinline__ void walk_rows_b(int b, const uint32_t* BMc, int T, uint32_t P, int Dm,
-                                            uint32_t* eb, int eoff) {
-  switch (b) {
-    case 2: walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    case 3: walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    case 4: walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    case 5: walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    case 6: walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    case 7: walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
-    default: walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eoff); break;
+// Depths with Dmax = DM <= 4 rows: the rows are unrolled at compile time and
+// the per-stage counts kept as level masks G[t] = {stages with count >= t+1}:
+// G[t] |= G[t-1] & R.  Level t+1 first becomes non-empty at row x exactly
+// when the maximum reaches t+1 there — the event (t+1, x).  Dmax = 2 (half
+// the depths at N = 256) costs one AND per word.
+template <int DM, int W, bool SMEM_EVT>
+__device__ __forceinline__ void walk_small(const uint32_t* BMc, int T, uint32_t P, uint32_t* eb,
+                                           int eoff) {
+  const uint32_t tail = P - 32u * (W - 1);
+  const uint32_t tmask = tail >= 32u ? 0xffffffffu : ((1u << tail) - 1u);
+  uint32_t G[DM][W];
+#pragma unroll
+  for (int x = 0; x < DM; ++x) {
+    const uint32_t pos = static_cast<uint32_t>(x) * P;
+    const uint32_t wi = pos >> 5, sh = pos & 31u;
+    uint32_t R[W];
+    uint32_t lo = BMc[wi * T];
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t hi = BMc[(wi + w + 1) * T];
+      R[w] = __funnelshift_r(lo, hi, sh);
+      lo = hi;
+    }
+    R[W - 1] &= tmask;
+#pragma unroll
+    for (int t = x; t >= 1; --t) {  // count >= t+1 is first possible at row t
+      uint32_t prior = 0, fresh = 0;  // G[t-1] is still the pre-row value here
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t old = (t < x) ? G[t][w] : 0u;
+        const uint32_t nv = G[t - 1][w] & R[w];
+        prior |= old;
+        fresh |= nv;
+        G[t][w] = old | nv;
+      }
+      if (prior == 0u && fresh != 0u) evt_add<SMEM_EVT>(eb, eoff + (t - 1) * DM + x);
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) G[0][w] = (x == 0 ? 0u : G[0][w]) | R[w];
   }
+}
+
+// (words per row, mode): mode = Dmax for Dmax <= 4 (walk_small), else
+// 8 + plane count (walk_rows).
+__device__ __forceinline__ int depth_class(const EntryDesc& e) {
+  const int W = (e.P + 31) >> 5;
+  const int mode = e.Dmax <= 4 ? e.Dmax : 8 + (32 - __clz(static_cast<uint32_t>(e.tmax)));
+  return (W << 5) | mode;
+}
+
+template <int W, bool SMEM_EVT>
+__device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0, int e1,
+                                         const uint32_t* BMc, int T, uint32_t* eb) {
+#define LP_RUN(CALL)                                                              \
+  for (int e = e0; e < e1; ++e) {                                                 \
+    const uint32_t P = static_cast<uint32_t>(ents[e].P);                          \
+    const int Dm = ents[e].Dmax, eo = ents[e].evt_off;                            \
+    (void)Dm;                                                                     \
+    CALL;                                                                         \
+  }                                                                               \
+  return;
+  switch (mode) {
+    case 2: LP_RUN((walk_small<2, W, SMEM_EVT>(BMc, T, P, eb, eo)))
+    case 3: LP_RUN((walk_small<3, W, SMEM_EVT>(BMc, T, P, eb, eo)))
+    case 4: LP_RUN((walk_small<4, W, SMEM_EVT>(BMc, T, P, eb, eo)))
+    case 10: LP_RUN((walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 11: LP_RUN((walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 12: LP_RUN((walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 13: LP_RUN((walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 14: LP_RUN((walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 15: LP_RUN((walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    default: LP_RUN((walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+  }
+#undef LP_RUN
 }
 
 }  // namespace
@@ -189,28 +251,30 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
     }
     if (own_h0 && k > 0) atomicAdd(&h0[s0], 1u);
 
-    for (int ei = 0; ei < ne; ++ei) {
-      const EntryDesc e = ents[ei];
-      const uint32_t P = static_cast<uint32_t>(e.P);
-      const int Dm = e.Dmax;
-      const int b = 32 - __clz(static_cast<uint32_t>(e.tmax));  // bits of tmax (>= 2)
-      const int eo = e.evt_off;
-      switch ((P + 31u) >> 5) {
-        case 1: walk_rows_b<1, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-        case 2: walk_rows_b<2, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-        case 3: walk_rows_b<3, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-        case 4: walk_rows_b<4, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+    // Depths come in ascending P, so (words per row, small-Dmax / plane
+    // count) classes form contiguous runs: dispatch once per run.
+    for (int ei = 0; ei < ne;) {
+      const int cls = depth_class(ents[ei]);
+      int ej = ei + 1;
+      while (ej < ne && depth_class(ents[ej]) == cls) ++ej;
+      const int W = cls >> 5, mode = cls & 31;
+      switch (W) {
+        case 1: walk_run<1, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+        case 2: walk_run<2, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+        case 3: walk_run<3, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+        case 4: walk_run<4, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
         default:
           if (WMAX > 4) {
-            switch ((P + 31u) >> 5) {
-              case 5: walk_rows_b<5, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-              case 6: walk_rows_b<6, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-              case 7: walk_rows_b<7, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
-              default: walk_rows_b<8, SMEM_EVT>(b, BMc, T, P, Dm, evt_base, eo); break;
+            switch (W) {
+              case 5: walk_run<5, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+              case 6: walk_run<6, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+              case 7: walk_run<7, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+              default: walk_run<8, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
             }
           }
           break;
       }
+      ei = ej;
     }
   }
   __syncthreads();
