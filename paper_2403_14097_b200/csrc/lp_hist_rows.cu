@@ -106,6 +106,54 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
   }
 }
 
+// One-word rows (P <= 32) and at most 64 of them: the bitmap streams
+// through a two-word window (refilled when the row start crosses a word —
+// a warp-uniform test, every lane walks the same depth), and the rows where
+// the maximum rose are kept as a 64-bit mask, so the row loop has no branch;
+// the events are emitted once after the walk.
+template <int B, bool SMEM_EVT>
+__device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t P, int Dm,
+                                           uint32_t* eb, int eoff) {
+  uint32_t Dp[B];
+#pragma unroll
+  for (int l = 0; l < B; ++l) Dp[l] = 0u;
+  const uint32_t tmask = P >= 32u ? 0xffffffffu : ((1u << P) - 1u);
+  uint32_t w0 = BMc[0], w1 = BMc[T];
+  const uint32_t* next = BMc + 2 * T;
+  uint32_t sh = 0;
+  unsigned long long rises = 0;
+  for (int x = 0; x < Dm; ++x) {
+    const uint32_t R = __funnelshift_r(w0, w1, sh) & tmask;
+    uint32_t z = 0;
+#pragma unroll
+    for (int l = 0; l < B; ++l) z |= Dp[l];
+    const uint32_t hit = R & ~z;
+    const uint32_t keep = hit ? 0u : 0xffffffffu;  // all-ones: decrement by R
+    rises |= static_cast<unsigned long long>(hit != 0u) << x;
+    uint32_t c = R ^ (~keep & tmask);
+#pragma unroll
+    for (int l = 0; l < B; ++l) {
+      const uint32_t t = (Dp[l] ^ keep) & c;
+      Dp[l] ^= c;
+      c = t;
+    }
+    sh += P;
+    if (sh >= 32u && x + 1 < Dm) {  // uniform across the warp; stays in the column
+      sh -= 32u;
+      w0 = w1;
+      w1 = *next;
+      next += T;
+    }
+  }
+  rises &= rises - 1;  // the first rise is t = 1 (h0's event)
+  int t = 2;
+  while (rises) {
+    const int x = __ffsll(rises) - 1;
+    rises &= rises - 1;
+    evt_add<SMEM_EVT>(eb, eoff + (t++ - 2) * Dm + x);
+  }
+}
+
 // Depths with Dmax = DM <= 4 rows: the rows are unrolled at compile time and
 // the per-stage counts kept as level masks G[t] = {stages with count >= t+1}:
 // G[t] |= G[t-1] & R.  Level t+1 first becomes non-empty at row x exactly
@@ -148,6 +196,13 @@ __device__ __forceinline__ void walk_small(const uint32_t* BMc, int T, uint32_t 
   }
 }
 
+template <int W, int B, bool SMEM_EVT>
+__device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P, int Dm,
+                                         uint32_t* eb, int eoff) {
+  if (W == 1 && Dm <= 64) walk_rows1<B, SMEM_EVT>(BMc, T, P, Dm, eb, eoff);
+  else walk_rows<W, B, SMEM_EVT>(BMc, T, P, Dm, eb, eoff);
+}
+
 // (words per row, mode): mode = Dmax for Dmax <= 4 (walk_small), else
 // 8 + plane count (walk_rows).
 __device__ __forceinline__ int depth_class(const EntryDesc& e) {
@@ -171,13 +226,13 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
     case 2: LP_RUN((walk_small<2, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 3: LP_RUN((walk_small<3, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 4: LP_RUN((walk_small<4, W, SMEM_EVT>(BMc, T, P, eb, eo)))
-    case 10: LP_RUN((walk_rows<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    case 11: LP_RUN((walk_rows<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    case 12: LP_RUN((walk_rows<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    case 13: LP_RUN((walk_rows<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    case 14: LP_RUN((walk_rows<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    case 15: LP_RUN((walk_rows<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    default: LP_RUN((walk_rows<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 10: LP_RUN((walk_gen<W, 2, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 11: LP_RUN((walk_gen<W, 3, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 12: LP_RUN((walk_gen<W, 4, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 13: LP_RUN((walk_gen<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 14: LP_RUN((walk_gen<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 15: LP_RUN((walk_gen<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    default: LP_RUN((walk_gen<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
   }
 #undef LP_RUN
 }
