@@ -1239,7 +1239,7 @@ lp_status lp_execute(lp_handle* h) {
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
   for (int j = 0; j < h->horizon; ++j) {
-    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, st, lv, cfg, pcost, histp, thr, throw_,
+    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, st, lv, cfg, pcost, histp, thr, throw_,
                               h->S, val, mig, par, stc, stm));
     ++launches;
   }

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "liveput.h"
 #include "lp_layout.h"
 
@@ -149,7 +151,7 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int src) {
 // One block per next-level node; threads stride over the prev nodes (each
 // keeps the first best in its own ascending order), then a warp-shuffle and a
 // cross-warp reduction pick (value desc, mig asc, index asc).
-__global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
+__global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __restrict__ levels,
                                                       const NodeCfg* __restrict__ cfg,
                                                       const double4* __restrict__ pcost,
                                                       const double* __restrict__ histp,
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(128) dp_step_kernel(int j, const LevelDesc* __
                                                       int32_t* __restrict__ parent,
                                                       double* __restrict__ stc,
                                                       double* __restrict__ stm) {
-  __shared__ Cand s_best[4];
+  __shared__ Cand s_best[16];
   const LevelDesc L = levels[j];
   if (static_cast<int>(blockIdx.x) >= L.next_count) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -328,13 +330,17 @@ __global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc
 }
 
 // ---------------------------------------------------------------------------
-cudaError_t launch_dp_step(int j, int next_count, cudaStream_t st, const LevelDesc* levels,
-                           const NodeCfg* cfg, const double4* pcost, const double* histp,
-                           const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
-                           double* val, double* mig, int32_t* parent, double* stc, double* stm) {
+cudaError_t launch_dp_step(int j, int next_count, int prev_count, cudaStream_t st,
+                           const LevelDesc* levels, const NodeCfg* cfg, const double4* pcost,
+                           const double* histp, const double* thr_tab, const int32_t* thr_row,
+                           const DpScalars& S, double* val, double* mig, int32_t* parent,
+                           double* stc, double* stm) {
   const int blocks = next_count;
   if (blocks <= 0) return cudaSuccess;
-  dp_step_kernel<<<blocks, 128, 0, st>>>(j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val,
+  // 128 threads per next node measured fastest (more threads per node cost
+  // more in the cross-warp reduction than the shorter phi chains save)
+  const int threads = std::min(128, std::max(32, (prev_count + 31) / 32 * 32));
+  dp_step_kernel<<<blocks, threads, 0, st>>>(j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val,
                                              mig, parent, stc, stm);
   return cudaGetLastError();
 }
