@@ -81,16 +81,34 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     return o;
   }
   const int dmax = min(L.k, pv.d);
+  // Terms that do not depend on m, computed once in the reference's order:
+  // the repartition cost (rollback when m == 0, or any depth change) is
+  // ((fixed + build) + update) + pipe (+ rollback penalty).
+  const double base = __dadd_rn(__dadd_rn(L.fixed, S.build), S.update);
+  const double c_pipe = __dadd_rn(base, nc.pipe);
+  const double c_rb = __dadd_rn(c_pipe, S.rollback);
+  const double te_pipe = __dsub_rn(S.T, c_pipe), te_rb = __dsub_rn(S.T, c_rb);
+  const double teff_pipe = (0.0 < te_pipe) ? te_pipe : 0.0;
+  const double teff_rb = (0.0 < te_rb) ? te_rb : 0.0;
+  const bool same_depth = nx.p == pv.p;
   double committed = 0.0, cost_sum = 0.0;
   for (int d = dmax; d >= 0; --d) {  // m = D - d ascending
     const double p = prob(d);
     if (p == 0.0) continue;
     const int m = pv.d - d;
-    bool rb;
-    double cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
-    if (rb) cost = __dadd_rn(cost, S.rollback);
-    const double te = __dsub_rn(S.T, cost);
-    const double t_eff = (0.0 < te) ? te : 0.0;
+    double cost, t_eff;
+    if (m == 0) {
+      cost = c_rb;
+      t_eff = teff_rb;
+    } else if (!same_depth) {
+      cost = c_pipe;
+      t_eff = teff_pipe;
+    } else {
+      bool rb;
+      cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
+      const double te = __dsub_rn(S.T, cost);
+      t_eff = (0.0 < te) ? te : 0.0;
+    }
     double rate = nc.thr;
     if (S.strict) {
       const int alive = min(nx.d, m);
