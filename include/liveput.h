@@ -157,6 +157,18 @@ void* lp_stream(lp_handle* h);
  *      max_bytes bounds the device store; when full it is dropped and refilled. */
 lp_status lp_set_hist_cache(lp_handle* h, int32_t enable, uint64_t max_bytes);
 
+/* ---- offline liveput tables ("sampling can be done
+ *      offline").  lp_precompute samples every config of n at
+ *      each (n[i], k[i]) into the device cache (turning the cache on), so a
+ *      later re-plan over those availability steps is DP-only.  The cache can
+ *      be serialised (lp_cache_export: call with buf = NULL for the size) and
+ *      restored into another handle with the same sampling options
+ *      (mc_trials, exact_cap, mc_seed); histograms do not depend on the
+ *      profile or the cost table. */
+lp_status lp_precompute(lp_handle* h, const int32_t* n, const int32_t* k, int32_t count);
+lp_status lp_cache_export(lp_handle* h, void* buf, uint64_t cap, uint64_t* len);
+lp_status lp_cache_import(lp_handle* h, const void* buf, uint64_t len);
+
 /* ---- Planner::phi (optimizer.hpp:57-58, optimizer.cpp:52-62, 96-138) ---- */
 lp_status lp_phi(lp_handle* h, lp_config prev, lp_config next, int32_t n_now, int32_t n_next,
                  double* committed, double* mig_cost_s);

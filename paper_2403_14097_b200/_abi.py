@@ -118,6 +118,9 @@ _SIGS = {
     "lp_get_stats": (C.c_int, [C.c_void_p, _P(lp_stats)]),
     "lp_stream": (C.c_void_p, [C.c_void_p]),
     "lp_set_hist_cache": (C.c_int, [C.c_void_p, C.c_int32, C.c_uint64]),
+    "lp_precompute": (C.c_int, [C.c_void_p, _P(C.c_int32), _P(C.c_int32), C.c_int32]),
+    "lp_cache_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, _P(C.c_uint64)]),
+    "lp_cache_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64]),
     "lp_phi": (C.c_int, [C.c_void_p, lp_config, lp_config, C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_double)]),
     "lp_sequence_value": (C.c_int, [C.c_void_p, lp_config, _P(lp_config), _P(C.c_int32), C.c_int32, _P(C.c_double)]),
     "lp_survivor_hist": (C.c_int, [C.c_void_p, lp_config, C.c_int32, C.c_int32, _P(C.c_uint64), _P(C.c_uint64)]),

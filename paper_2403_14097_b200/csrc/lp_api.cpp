@@ -1300,6 +1300,126 @@ lp_status lp_set_hist_cache(lp_handle* h, int32_t enable, uint64_t max_bytes) {
   return LP_OK;
 }
 
+// Offline tables: each (n, k) is staged through a one-interval re-plan
+// [n, n, n - k] from suspension, whose level 1 needs every config of n at k.
+lp_status lp_precompute(lp_handle* h, const int32_t* ns, const int32_t* ks, int32_t count) {
+  if (!h || (count > 0 && (!ns || !ks))) return fail(h, LP_EINVAL, "lp_precompute: bad argument");
+  if (!h->cache_on) {
+    h->cache_on = true;
+    h->store_idx.clear();
+    h->store_used = 0;
+  }
+  for (int i = 0; i < count; ++i) {
+    if (ns[i] < 0 || ks[i] < 0 || ks[i] > ns[i])
+      return fail(h, LP_EINVAL, "lp_precompute: need 0 <= k <= n (got n=%d k=%d)", ns[i], ks[i]);
+    const int32_t seq[3] = {ns[i], ns[i], ns[i] - ks[i]};
+    lp_status s = lp_prepare(h, lp_config{0, 0}, seq, 3);
+    if (s != LP_OK) return s;
+    s = lp_execute(h);
+    if (s != LP_OK) return s;
+  }
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  h->prepared = false;
+  return LP_OK;
+}
+
+namespace {
+constexpr uint32_t kCacheMagic = 0x3143504cu;  // "LPC1"
+struct CacheHeader {
+  uint32_t magic;
+  int32_t mc_trials;
+  uint64_t exact_cap;
+  uint64_t mc_seed;
+  uint64_t slots;
+};
+struct SlotHeader {
+  int32_t n, k;
+  uint64_t count;
+  int32_t entries, pad;
+};
+struct EntryHeader {
+  int32_t P, Dmax;
+  int64_t len;
+};
+}  // namespace
+
+// Serialises the device histogram store: probabilities depend only on
+// (n, k) and the sampling options, never on the profile or costs.
+lp_status lp_cache_export(lp_handle* h, void* buf, uint64_t cap, uint64_t* len) {
+  if (!h || !len) return fail(h, LP_EINVAL, "lp_cache_export: bad argument");
+  uint64_t need = sizeof(CacheHeader);
+  for (const auto& [key, slot] : h->store_idx) {
+    need += sizeof(SlotHeader);
+    for (const auto& [P, v] : slot.ents)
+      need += sizeof(EntryHeader) + sizeof(double) * hist_row(v.first + 1, key.second);
+  }
+  *len = need;
+  if (!buf) return LP_OK;
+  if (cap < need) return fail(h, LP_EINVAL, "lp_cache_export: buffer of %llu bytes, need %llu",
+                              (unsigned long long)cap, (unsigned long long)need);
+  LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  unsigned char* o = static_cast<unsigned char*>(buf);
+  CacheHeader ch{kCacheMagic, h->opt.mc_trials, h->opt.exact_cap, h->opt.mc_seed,
+                 (uint64_t)h->store_idx.size()};
+  std::memcpy(o, &ch, sizeof ch);
+  o += sizeof ch;
+  for (const auto& [key, slot] : h->store_idx) {
+    SlotHeader sh{key.first, key.second, slot.count, (int32_t)slot.ents.size(), 0};
+    std::memcpy(o, &sh, sizeof sh);
+    o += sizeof sh;
+    for (const auto& [P, v] : slot.ents) {
+      const int64_t rows = hist_row(v.first + 1, key.second);
+      EntryHeader eh{P, v.first, rows};
+      std::memcpy(o, &eh, sizeof eh);
+      o += sizeof eh;
+      LP_CUDA(h, cudaMemcpy(o, static_cast<double*>(h->store.p) + v.second, sizeof(double) * rows,
+                            cudaMemcpyDeviceToHost));
+      o += sizeof(double) * rows;
+    }
+  }
+  return LP_OK;
+}
+
+lp_status lp_cache_import(lp_handle* h, const void* buf, uint64_t len) {
+  if (!h || !buf || len < sizeof(CacheHeader)) return fail(h, LP_EINVAL, "lp_cache_import: bad buffer");
+  const unsigned char* p = static_cast<const unsigned char*>(buf);
+  const unsigned char* end = p + len;
+  CacheHeader ch;
+  std::memcpy(&ch, p, sizeof ch);
+  p += sizeof ch;
+  if (ch.magic != kCacheMagic) return fail(h, LP_EINVAL, "lp_cache_import: not a liveput table");
+  if (ch.mc_trials != h->opt.mc_trials || ch.exact_cap != h->opt.exact_cap ||
+      ch.mc_seed != h->opt.mc_seed)
+    return fail(h, LP_EINVAL, "lp_cache_import: table was sampled with different PlannerOptions "
+                              "(mc_trials/exact_cap/mc_seed)");
+  h->cache_on = true;
+  for (uint64_t s = 0; s < ch.slots; ++s) {
+    if (p + sizeof(SlotHeader) > end) return fail(h, LP_EINVAL, "lp_cache_import: truncated");
+    SlotHeader sh;
+    std::memcpy(&sh, p, sizeof sh);
+    p += sizeof sh;
+    auto& slot = h->store_idx[{sh.n, sh.k}];
+    slot.count = sh.count;
+    for (int e = 0; e < sh.entries; ++e) {
+      if (p + sizeof(EntryHeader) > end) return fail(h, LP_EINVAL, "lp_cache_import: truncated");
+      EntryHeader eh;
+      std::memcpy(&eh, p, sizeof eh);
+      p += sizeof eh;
+      if (eh.len != hist_row(eh.Dmax + 1, sh.k) || p + sizeof(double) * eh.len > end)
+        return fail(h, LP_EINVAL, "lp_cache_import: corrupt entry");
+      lp_status gs = grow_store(h, h->store_used + eh.len);
+      if (gs != LP_OK) return gs;
+      LP_CUDA(h, cudaMemcpy(static_cast<double*>(h->store.p) + h->store_used, p,
+                            sizeof(double) * eh.len, cudaMemcpyHostToDevice));
+      slot.ents[eh.P] = {eh.Dmax, (int)h->store_used};
+      h->store_used += eh.len;
+      p += sizeof(double) * eh.len;
+    }
+  }
+  h->prepared = false;
+  return LP_OK;
+}
+
 lp_status lp_get_stats(const lp_handle* hc, lp_stats* out) {
   lp_handle* h = const_cast<lp_handle*>(hc);
   if (!h || !out) return fail(h, LP_EINVAL, "null argument");

@@ -166,6 +166,24 @@ class Planner:
         """Reuse (n, k) ensembles across re-plans, like the reference's hist_cache_."""
         _abi.check(self._lib.lp_set_hist_cache(self._h, int(enable), max_bytes), self._h)
 
+    def precompute(self, pairs) -> None:
+        """Offline liveput tables: sample every config of n at each (n, k)."""
+        pairs = list(pairs)
+        ns = (C.c_int32 * max(len(pairs), 1))(*[p[0] for p in pairs])
+        ks = (C.c_int32 * max(len(pairs), 1))(*[p[1] for p in pairs])
+        _abi.check(self._lib.lp_precompute(self._h, ns, ks, len(pairs)), self._h)
+
+    def export_tables(self) -> bytes:
+        n = C.c_uint64()
+        _abi.check(self._lib.lp_cache_export(self._h, None, 0, C.byref(n)), self._h)
+        buf = (C.c_uint8 * n.value)()
+        _abi.check(self._lib.lp_cache_export(self._h, buf, n.value, C.byref(n)), self._h)
+        return bytes(buf)
+
+    def import_tables(self, data: bytes) -> None:
+        buf = (C.c_uint8 * len(data)).from_buffer_copy(data)
+        _abi.check(self._lib.lp_cache_import(self._h, buf, len(data)), self._h)
+
     def stream_ptr(self) -> int:
         return self._lib.lp_stream(self._h) or 0
 

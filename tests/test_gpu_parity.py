@@ -301,3 +301,29 @@ def test_hist_cache_reuses_ensembles():
     assert first.cached_pairs == 0 and first.mc_pairs > 0
     assert second.mc_pairs == 0 and second.cached_pairs > 0  # everything came from the cache
     p.close()
+
+
+def test_offline_tables_roundtrip():
+    """precompute (n, k) tables, export, import into a fresh
+    handle: the re-plan is DP-only and identical to a cold one."""
+    w = lm_1p5b()
+    opt = PlannerOptions(mc_trials=5000)
+    ns = [96, 90, 90, 84, 88, 80]
+    pairs = sorted({(ns[j], max(0, ns[j] - ns[j + 1])) for j in range(len(ns) - 1)})
+    a = planner(w, opt)
+    a.precompute(pairs)
+    blob = a.export_tables()
+    assert blob[:4] == b"LPC1" and len(blob) > 1000
+    b = planner(w, opt)
+    b.import_tables(blob)
+    cur = ParallelConfig(12, 8)
+    warm = b.dp_optimize(cur, ns)
+    st = b.stats()
+    cold = planner(w, opt).dp_optimize(cur, ns)
+    assert plan_rows(warm) == plan_rows(cold)
+    assert st.cached_pairs >= 1 and st.mc_pairs <= 1  # only level 0 (current) may need sampling
+    c = planner(w, PlannerOptions(mc_trials=5001))
+    with pytest.raises(ValueError):
+        c.import_tables(blob)
+    for p in (a, b, c):
+        p.close()
