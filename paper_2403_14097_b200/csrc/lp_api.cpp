@@ -95,6 +95,59 @@ struct Packer {
   }
 };
 
+// Small-integer-keyed map (keys are depths P <= n): a dense vector with
+// presence flags, iterated in ascending key order like std::map, without a
+// node allocation per depth on the re-plan path.
+template <class V>
+class DenseMap {
+ public:
+  struct iterator {
+    const DenseMap* m;
+    int k;
+    std::pair<int, const V&> operator*() const { return {k, m->val_[k]}; }
+    iterator& operator++() {
+      ++k;
+      skip();
+      return *this;
+    }
+    void skip() {
+      while (k < (int)m->has_.size() && !m->has_[k]) ++k;
+    }
+    bool operator!=(const iterator& o) const { return k != o.k; }
+  };
+  V& operator[](int k) {
+    if (k >= (int)val_.size()) {
+      val_.resize(k + 1);
+      has_.resize(k + 1, 0);
+    }
+    if (!has_[k]) {
+      has_[k] = 1;
+      ++cnt_;
+      val_[k] = V{};
+    }
+    return val_[k];
+  }
+  const V* find(int k) const { return (k >= 0 && k < (int)has_.size() && has_[k]) ? &val_[k] : nullptr; }
+  void erase(int k) {
+    if (find(k)) {
+      has_[k] = 0;
+      --cnt_;
+    }
+  }
+  size_t size() const { return (size_t)cnt_; }
+  iterator begin() const {
+    iterator it{this, 0};
+    it.skip();
+    return it;
+  }
+  iterator end() const { return iterator{this, (int)has_.size()}; }
+
+ private:
+  std::vector<V> val_;
+  std::vector<uint8_t> has_;
+  int cnt_ = 0;
+};
+
 // ---------------------------------------------------------------------------
 // histogram plan: ensembles -> pairs / entries / work items / launch groups
 struct EnsembleSpec {
@@ -102,7 +155,7 @@ struct EnsembleSpec {
   bool exact = false;
   uint64_t count = 0;  // ensemble size (all ranks)
   uint64_t seed = 0;
-  std::map<int, int> dmax_by_p;  // depth -> largest D needed
+  DenseMap<int> dmax_by_p;       // depth -> largest D needed
   uint64_t ref_keys = 0;         // distinct (D,P) keys the reference would tally
 };
 
@@ -661,6 +714,19 @@ struct lp_handle {
   PinBuf pin_up, pin_down;
   size_t up_bytes = 0;
   lp_stats stats{};
+  // DP tables: a second image, so lp_replan can build and upload them while
+  // the histogram kernels run
+  DevBuf tables2;
+  PinBuf pin_up2;
+  cudaEvent_t ev_up[2] = {nullptr, nullptr};  // last upload out of pin_up / pin_up2
+  struct PrepState {
+    int len = 0;
+    std::vector<int32_t> n_seq;
+    std::vector<int> lbase, lcount, level_spec;
+    std::vector<EnsembleSpec> specs;
+    size_t fresh = 0;
+    double host_ms = 0.0;
+  } ps;
 
   // ensemble calls (phi / survivor_hist / liveput) and their cache
   DevBuf e_tables, e_work;
@@ -669,7 +735,7 @@ struct lp_handle {
   // device histogram store (FP64 probabilities, see lp_prepare)
   struct StoreSlot {
     uint64_t count = 0;                         // ensemble size
-    std::map<int, std::pair<int, int>> ents;    // P -> (Dmax, store offset of D = 1)
+    DenseMap<std::pair<int, int>> ents;         // P -> (Dmax, store offset of D = 1)
   };
   bool cache_on = false;
   uint64_t cache_max = 4ull << 30;              // bytes
@@ -900,6 +966,7 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
+  for (auto& ev : h->ev_up) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = h;
   return LP_OK;
@@ -911,6 +978,8 @@ void lp_destroy(lp_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->comm) nccl().CommDestroy(h->comm);
   for (auto& ev : h->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->ev_up)
     if (ev) cudaEventDestroy(ev);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -924,11 +993,64 @@ lp_status lp_get_options(const lp_handle* h, lp_options* out) {
 
 void* lp_stream(lp_handle* h) { return h ? (void*)h->stream : nullptr; }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------------------
-// prepare: levels (optimizer.cpp:148-183), ensembles, tables; one H2D copy.
-lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len) {
+namespace {
+
+struct Section {
+  const void* src;
+  size_t bytes;
+  size_t* off;  // receives the section's offset in the image
+};
+
+template <typename T>
+Section sec(const std::vector<T>& v, size_t* off) {
+  return {v.data(), v.size() * sizeof(T), off};
+}
+
+// Lays the sections out (256-byte aligned) straight into the pinned staging
+// buffer and uploads them with one copy on the handle's stream.  `done`
+// marks the previous upload out of `pin`, which must finish before the
+// staging memory is rewritten.
+lp_status upload_image(lp_handle* h, std::initializer_list<Section> secs, DevBuf& dst, PinBuf& pin,
+                       cudaEvent_t done, size_t* total) {
+  size_t o = 0;
+  for (const Section& x : secs) {
+    *x.off = o;
+    o += (std::max<size_t>(x.bytes, 1) + 255) & ~size_t(255);
+  }
+  LP_CUDA(h, cudaEventSynchronize(done));
+  LP_CUDA(h, pin.ensure(o));
+  LP_CUDA(h, dst.ensure(o));
+  unsigned char* base = static_cast<unsigned char*>(pin.p);
+  for (const Section& x : secs)
+    if (x.bytes) std::memcpy(base + *x.off, x.src, x.bytes);
+  LP_CUDA(h, cudaMemcpyAsync(dst.p, pin.p, o, cudaMemcpyHostToDevice, h->stream));
+  LP_CUDA(h, cudaEventRecord(done, h->stream));
+  *total = o;
+  return LP_OK;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+
+bool trace_prepare() {
+  static const bool on = getenv("LIVEPUT_TRACE_PREPARE") != nullptr;
+  return on;
+}
+
+// prepare, part 1: levels (optimizer.cpp:148-183), ensembles and the
+// histogram plan; uploads the histogram image and sizes the work arena.
+lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len) {
   if (!h) return fail(nullptr, LP_EINVAL, "null handle");
   const auto t_start = std::chrono::steady_clock::now();
+  const bool trace = trace_prepare();
+  auto mark = [&](const char* what) {
+    if (trace) fprintf(stderr, "[prepare] %-10s %8.3f ms\n", what, ms_since(t_start));
+  };
+  h->prepared = false;  // until prepare_dp has run
   if (!n_seq || len < 2) return fail(h, LP_EINVAL, "dp_optimize: need at least N_i and N_{i+1}");
   cudaSetDevice(h->device);
   for (int i = 0; i < len; ++i) {
@@ -960,6 +1082,7 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     h->cfg.push_back({0, 0, -1, 0});  // suspension is always reachable
     lcount[j] = (int)h->cfg.size() - lbase[j];
   }
+  mark("levels");
   // ensembles: one per distinct (n_now, k) whose histograms phi will read.
   // Level j >= 1 needs every config of n_now (all D <= n/P of each feasible
   // P); level 0 needs only `current`.
@@ -1033,8 +1156,8 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
       bool covered = it != h->store_idx.end();
       if (covered)
         for (const auto& [P, Dm] : specs[si].dmax_by_p) {
-          auto e = it->second.ents.find(P);
-          if (e == it->second.ents.end() || e->second.first < Dm) covered = false;
+          const auto* e = it->second.ents.find(P);
+          if (!e || e->first < Dm) covered = false;
         }
       if (covered) continue;
       EnsembleSpec sp = specs[si];
@@ -1049,9 +1172,11 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     }
     if (h->store_used + need <= h->cache_max / 8 || pass == 1) break;  // else evict all, retry
   }
+  mark("specs");
   std::string err;
   lp_status s = build_hist_plan(fresh, h->rank, h->nranks, h->hp, err, h->num_sms);
   if (s != LP_OK) return fail(h, s, "%s", err.c_str());
+  mark("histplan");
   // store slots of the fresh entries (appended; old slots of recomputed
   // ensembles are abandoned until the next eviction)
   h->store_off.assign(h->hp.entries.size(), 0);
@@ -1065,17 +1190,85 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
   for (const PairDesc& pd : h->hp.pairs) {
     auto& slot = h->store_idx[{pd.n, pd.k}];
     slot.count = pd.count;
-    for (auto it = slot.ents.begin(); it != slot.ents.end();) {  // drop stale depth slots
-      bool fresh_p = false;
-      for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e)
-        fresh_p |= h->hp.entries[e].P == it->first;
-      it = fresh_p ? std::next(it) : slot.ents.erase(it);
-    }
+    std::vector<uint8_t> fresh_p(pd.n + 2, 0);  // drop stale depth slots
+    for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e) fresh_p[h->hp.entries[e].P] = 1;
+    std::vector<int> stale;
+    for (const auto& [P, v] : slot.ents)
+      if (P >= (int)fresh_p.size() || !fresh_p[P]) stale.push_back(P);
+    for (int P : stale) slot.ents.erase(P);
   }
   {
     lp_status gs = grow_store(h, h->store_used);
     if (gs != LP_OK) return gs;
   }
+  mark("store");
+  {
+    size_t bytes = 0;
+    lp_status us = upload_image(h,
+                                {sec(h->hp.pairs, &h->off_pairs), sec(h->hp.entries, &h->off_entries),
+                                 sec(h->hp.draws, &h->off_draws), sec(h->hp.binom, &h->off_binom),
+                                 sec(h->hp.work, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
+                                 sec(h->store_off, &h->off_store_off)},
+                                h->tables, h->pin_up, h->ev_up[0], &bytes);
+    if (us != LP_OK) return us;
+    h->up_bytes = bytes;
+  }
+  // work arena: histogram scratch and the DP state of every node
+  const size_t nn = h->cfg.size();
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
+  h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
+  h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
+  h->w_val = take(8 * nn);
+  h->w_mig = take(8 * nn);
+  h->w_par = take(4 * nn);
+  h->w_stc = take(8 * nn);
+  h->w_stm = take(8 * nn);
+  h->w_plan = take(sizeof(lp_plan_step) * H);
+  h->w_live = take(sizeof(lp_liveput_row) * std::max<size_t>(nn, 1));  // >= liveput rows
+  h->w_final = take(8);
+  LP_CUDA(h, h->work.ensure(o));
+  mark("upload1");
+  std::memset(&h->stats, 0, sizeof h->stats);
+  h->stats.resolutions = h->hp.resolutions;
+  h->stats.scenarios = h->hp.scenarios;
+  h->stats.local_scenarios = h->hp.local_scenarios;
+  h->stats.mc_pairs = h->hp.mc_pairs;
+  h->stats.exact_pairs = h->hp.exact_pairs;
+  h->stats.horizon = H;
+  h->stats.hist_alg_ops = h->hp.alg_ops;
+  h->stats.cached_pairs = specs.size() - fresh.size();
+  auto& ps = h->ps;
+  ps.len = len;
+  ps.n_seq.assign(n_seq, n_seq + len);
+  ps.lbase = std::move(lbase);
+  ps.lcount = std::move(lcount);
+  ps.level_spec = std::move(level_spec);
+  ps.specs = std::move(specs);
+  ps.fresh = fresh.size();
+  ps.host_ms = ms_since(t_start);
+  return LP_OK;
+}
+
+// prepare, part 2: node rows, throughput / cost tables, liveput rows and the
+// DP scalars; uploads the DP image.
+lp_status prepare_dp(lp_handle* h) {
+  const auto t_start = std::chrono::steady_clock::now();
+  const bool trace = trace_prepare();
+  auto mark = [&](const char* what) {
+    if (trace) fprintf(stderr, "[prepare] %-10s %8.3f ms\n", what, ms_since(t_start));
+  };
+  const int H = h->horizon;
+  const int32_t* n_seq = h->ps.n_seq.data();
+  const std::vector<int>& lbase = h->ps.lbase;
+  const std::vector<int>& lcount = h->ps.lcount;
+  const std::vector<int>& level_spec = h->ps.level_spec;
+  const std::vector<EnsembleSpec>& specs = h->ps.specs;
   // node histogram rows + levels
   std::map<int, int> thr_need;
   int pmax = 1;
@@ -1128,7 +1321,9 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
       thr_need[p] = need_d[p];
       pmax = std::max(pmax, p);
     }
+  mark("nodes");
   build_thr(h->model, thr_need, pmax, h->thr);
+  mark("thr");
   // liveput rows
   h->lrows.clear();
   for (int j = 0; j < H; ++j) {
@@ -1140,67 +1335,26 @@ lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int3
     }
   }
   h->S = dp_scalars(h, H);
-  // ---- pack + upload
-  Packer pk;
-  h->off_pairs = pk.add(h->hp.pairs);
-  h->off_entries = pk.add(h->hp.entries);
-  h->off_draws = pk.add(h->hp.draws);
-  h->off_binom = pk.add(h->hp.binom);
-  h->off_work = pk.add(h->hp.work);
-  h->off_divtab = pk.add(h->hp.divtab);
-  h->off_levels = pk.add(h->levels);
-  h->off_cfg = pk.add(h->cfg);
-  h->off_cost = pk.add(h->pcost);
-  h->off_lrows = pk.add(h->lrows);
-  h->off_thr = pk.add(h->thr.vals);
-  h->off_throw = pk.add(h->thr.row);
-  h->off_store_off = pk.add(h->store_off);
-  LP_CUDA(h, h->tables.ensure(pk.bytes.size()));
-  LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
-  std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
-  LP_CUDA(h, cudaMemcpyAsync(h->tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
-                             h->stream));
-  h->up_bytes = pk.bytes.size();
-  // work arena
-  const size_t nn = h->cfg.size();
-  size_t o = 0;
-  auto take = [&](size_t bytes) {
-    size_t r = o;
-    o += (bytes + 255) & ~size_t(255);
-    return r;
-  };
-  h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
-  h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
-  h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
-  h->w_val = take(8 * nn);
-  h->w_mig = take(8 * nn);
-  h->w_par = take(4 * nn);
-  h->w_stc = take(8 * nn);
-  h->w_stm = take(8 * nn);
-  h->w_plan = take(sizeof(lp_plan_step) * H);
-  h->w_live = take(sizeof(lp_liveput_row) * std::max<size_t>(h->lrows.size(), 1));
-  h->w_final = take(8);
-  LP_CUDA(h, h->work.ensure(o));
+  mark("lrows");
+  size_t bytes = 0;
+  lp_status us = upload_image(h,
+                              {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
+                               sec(h->pcost, &h->off_cost), sec(h->lrows, &h->off_lrows),
+                               sec(h->thr.vals, &h->off_thr), sec(h->thr.row, &h->off_throw)},
+                              h->tables2, h->pin_up2, h->ev_up[1], &bytes);
+  if (us != LP_OK) return us;
+  mark("upload2");
+  h->up_bytes += bytes;
   h->prepared = true;
-  std::memset(&h->stats, 0, sizeof h->stats);
-  h->stats.resolutions = h->hp.resolutions;
-  h->stats.scenarios = h->hp.scenarios;
-  h->stats.local_scenarios = h->hp.local_scenarios;
-  h->stats.mc_pairs = h->hp.mc_pairs;
-  h->stats.exact_pairs = h->hp.exact_pairs;
-  h->stats.horizon = H;
-  h->stats.hist_alg_ops = h->hp.alg_ops;
-  h->stats.h2d_bytes = pk.bytes.size() + sizeof(int32_t) * len;
-  h->stats.cached_pairs = specs.size() - fresh.size();
-  h->stats.prepare_ms =
-      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  h->stats.h2d_bytes = h->up_bytes + sizeof(int32_t) * h->ps.len;
+  h->ps.host_ms += ms_since(t_start);
+  h->stats.prepare_ms = h->ps.host_ms;
   return LP_OK;
 }
 
-lp_status lp_execute(lp_handle* h) {
-  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
-  if (!h->prepared) return fail(h, LP_EINVAL, "lp_execute: call lp_prepare first");
-  cudaSetDevice(h->device);
+// execute, part 1: histogram kernels, the cross-rank sum, normalisation
+// into the probability store.  Needs only prepare_hist's image.
+lp_status exec_hist(lp_handle* h) {
   cudaStream_t st = h->stream;
   HistDev d{};
   d.pairs = dptr<PairDesc>(h->tables, h->off_pairs);
@@ -1222,20 +1376,28 @@ lp_status lp_execute(lp_handle* h) {
     if (r != ncclSuccess) return fail(h, LP_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(r));
   }
   LP_CUDA(h, cudaEventRecord(h->ev[2], st));
-  const LevelDesc* lv = dptr<LevelDesc>(h->tables, h->off_levels);
-  const NodeCfg* cfg = dptr<NodeCfg>(h->tables, h->off_cfg);
-  const double4* pcost = dptr<double4>(h->tables, h->off_cost);
-  const double* thr = dptr<double>(h->tables, h->off_thr);
-  const int32_t* throw_ = dptr<int32_t>(h->tables, h->off_throw);
+  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
+                              dptr<int32_t>(h->tables, h->off_store_off),
+                              static_cast<double*>(h->store.p)));
+  h->stats.kernel_launches = launches + 1;
+  return LP_OK;
+}
+
+// execute, part 2: the lookahead DP, traceback and liveput rows.
+lp_status exec_dp(lp_handle* h) {
+  cudaStream_t st = h->stream;
+  int launches = 0;
+  const LevelDesc* lv = dptr<LevelDesc>(h->tables2, h->off_levels);
+  const NodeCfg* cfg = dptr<NodeCfg>(h->tables2, h->off_cfg);
+  const double4* pcost = dptr<double4>(h->tables2, h->off_cost);
+  const double* thr = dptr<double>(h->tables2, h->off_thr);
+  const int32_t* throw_ = dptr<int32_t>(h->tables2, h->off_throw);
   double* val = dptr<double>(h->work, h->w_val);
   double* mig = dptr<double>(h->work, h->w_mig);
   int32_t* par = dptr<int32_t>(h->work, h->w_par);
   double* stc = dptr<double>(h->work, h->w_stc);
   double* stm = dptr<double>(h->work, h->w_stm);
   double* histp = static_cast<double*>(h->store.p);
-  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
-                              dptr<int32_t>(h->tables, h->off_store_off), histp));
-  ++launches;
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
   for (int j = 0; j < h->horizon; ++j) {
@@ -1248,14 +1410,31 @@ lp_status lp_execute(lp_handle* h) {
                              dptr<double>(h->work, h->w_final)));
   ++launches;
   if (!h->lrows.empty()) {
-    LP_CUDA(h, launch_liveput((int)h->lrows.size(), st, dptr<int4>(h->tables, h->off_lrows), lv,
+    LP_CUDA(h, launch_liveput((int)h->lrows.size(), st, dptr<int4>(h->tables2, h->off_lrows), lv,
                               cfg, nullptr, histp, thr, throw_,
                               dptr<lp_liveput_row>(h->work, h->w_live)));
     ++launches;
   }
   LP_CUDA(h, cudaEventRecord(h->ev[3], st));
-  h->stats.kernel_launches = launches;
+  h->stats.kernel_launches += launches;
   return LP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lp_status lp_prepare(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len) {
+  lp_status s = prepare_hist(h, current, n_seq, len);
+  return s != LP_OK ? s : prepare_dp(h);
+}
+
+lp_status lp_execute(lp_handle* h) {
+  if (!h) return fail(nullptr, LP_EINVAL, "null handle");
+  if (!h->prepared) return fail(h, LP_EINVAL, "lp_execute: call lp_prepare first");
+  cudaSetDevice(h->device);
+  lp_status s = exec_hist(h);
+  return s != LP_OK ? s : exec_dp(h);
 }
 
 lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_t cap,
@@ -1283,9 +1462,12 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_
 
 lp_status lp_replan(lp_handle* h, lp_config current, const int32_t* n_seq, int32_t len,
                     lp_plan_step* out, lp_liveput_row* live, int32_t cap, int32_t* rows) {
-  lp_status s = lp_prepare(h, current, n_seq, len);
-  if (s != LP_OK) return s;
-  s = lp_execute(h);
+  // The histogram kernels are launched before the DP tables are built, so
+  // the host half of the preparation runs under the device's histogram time.
+  lp_status s = prepare_hist(h, current, n_seq, len);
+  if (s == LP_OK) s = exec_hist(h);
+  if (s == LP_OK) s = prepare_dp(h);
+  if (s == LP_OK) s = exec_dp(h);
   if (s != LP_OK) return s;
   return lp_fetch(h, out, live, cap, rows);
 }
