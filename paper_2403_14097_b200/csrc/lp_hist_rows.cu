@@ -196,6 +196,41 @@ __device__ __forceinline__ void walk_small(const uint32_t* BMc, int T, uint32_t 
   }
 }
 
+// Few stages (P <= 16) and many rows (10..64): visit the sorted,
+// register-resident slots instead of the rows.  Per-stage counts are nibbles
+// of one 64-bit word; with k <= 16 a count can only reach 16 on the last
+// slot, after its comparison, so the carry into the next nibble is never
+// read.  A slot (x, r) raises the maximum exactly when its stage's count
+// equals it; the rows where that happened are kept as a mask and the events
+// emitted after the walk, as in walk_rows1.  Branch-free: slots past lim
+// (and the 0xffffffff padding) count nothing.
+template <int KS, bool P1, bool SMEM_EVT>
+__device__ __forceinline__ void walk_elems(const uint32_t (&s)[KS], uint32_t P, uint32_t magic,
+                                           uint32_t lim, int Dm, uint32_t* eb, int eo) {
+  unsigned long long cnt = 0ull, rises = 0ull;
+  uint32_t mx = 0;
+  const uint32_t negP = 0u - P;
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {
+    const uint32_t v = s[i];
+    const uint32_t q = P1 ? v : __umulhi(v, magic);
+    const uint32_t sh = (v + q * negP) << 2;
+    const uint32_t c = static_cast<uint32_t>(cnt >> sh) & 15u;
+    const bool hit = v < lim && c == mx;
+    mx += hit ? 1u : 0u;
+    rises |= static_cast<unsigned long long>(hit) << (q & 63u);
+    // slots are sorted, so the ones past lim come last: counting them is harmless
+    cnt += 1ull << sh;
+  }
+  rises &= rises - 1;  // the first rise is t = 1 (h0's event)
+  int t = 2;
+  while (rises) {
+    const int x = __ffsll(rises) - 1;
+    rises &= rises - 1;
+    evt_add<SMEM_EVT>(eb, eo + (t++ - 2) * Dm + x);
+  }
+}
+
 template <int W, int B, bool SMEM_EVT>
 __device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P, int Dm,
                                          uint32_t* eb, int eoff) {
@@ -203,17 +238,21 @@ __device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P,
   else walk_rows<W, B, SMEM_EVT>(BMc, T, P, Dm, eb, eoff);
 }
 
-// (words per row, mode): mode = Dmax for Dmax <= 4 (walk_small), else
-// 8 + plane count (walk_rows).
+// (words per row, mode): mode = Dmax for Dmax <= 4 (walk_small), 5 for the
+// slot walk (ELEMS: k <= 16 slots in registers; P <= 16 and >= 10 rows),
+// else 8 + plane count (walk_rows).
+template <bool ELEMS>
 __device__ __forceinline__ int depth_class(const EntryDesc& e) {
   const int W = (e.P + 31) >> 5;
+  if (ELEMS && e.P <= 16 && e.Dmax >= 10 && e.Dmax <= 64) return (1 << 5) | 5;
   const int mode = e.Dmax <= 4 ? e.Dmax : 8 + (32 - __clz(static_cast<uint32_t>(e.tmax)));
   return (W << 5) | mode;
 }
 
-template <int W, bool SMEM_EVT>
+template <int W, bool SMEM_EVT, int KS>
 __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0, int e1,
-                                         const uint32_t* BMc, int T, uint32_t* eb) {
+                                         const uint32_t* BMc, int T, uint32_t* eb,
+                                         const uint32_t (&sl)[KS]) {
 #define LP_RUN(CALL)                                                              \
   for (int e = e0; e < e1; ++e) {                                                 \
     const uint32_t P = static_cast<uint32_t>(ents[e].P);                          \
@@ -223,6 +262,20 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
   }                                                                               \
   return;
   switch (mode) {
+    case 5:
+      if (W == 1 && KS > 1) {
+        for (int e = e0; e < e1; ++e) {
+          const EntryDesc& x = ents[e];
+          const uint32_t P = static_cast<uint32_t>(x.P);
+          if (P == 1u)
+            walk_elems<KS, true, SMEM_EVT>(sl, P, 0u, static_cast<uint32_t>(x.lim), x.Dmax, eb, x.evt_off);
+          else
+            walk_elems<KS, false, SMEM_EVT>(sl, P, x.magic, static_cast<uint32_t>(x.lim), x.Dmax, eb,
+                                            x.evt_off);
+        }
+        return;
+      }
+      break;
     case 2: LP_RUN((walk_small<2, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 3: LP_RUN((walk_small<3, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 4: LP_RUN((walk_small<4, W, SMEM_EVT>(BMc, T, P, eb, eo)))
@@ -281,11 +334,18 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   uint32_t* evt_base = SMEM_EVT ? evt : evt_g + w.evt_lo;
   uint32_t* BMc = BM + tid;
 
+  constexpr int KS = KREG > 0 ? KREG : 1;
   for (uint64_t t = w.t0 + tid; t < w.t1; t += T) {
     uint32_t s0 = 0;
+    uint32_t sl[KS];  // KREG > 0: the sorted slots (padding 0xffffffff)
     for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
-    if (KREG > 0 && !pd.exact) {
-      s0 = gen_mc_bitmap<(KREG > 0 ? KREG : 1)>(pd.seed, t, k, dc, BMc, T);
+    if (KREG > 0) {
+      if (pd.exact) gen_exact_regs<KS>(t, n, k, binom + pd.binom_off, pd.binom_stride, sl);
+      else gen_mc_regs<KS>(pd.seed, t, k, dc, sl);
+#pragma unroll
+      for (int i = 0; i < KS; ++i)
+        if (sl[i] != 0xffffffffu) BMc[(sl[i] >> 5) * T] |= 1u << (sl[i] & 31);
+      s0 = sl[0];
     } else if (pd.exact) {
       uint64_t rank = t;
       int c = 0;
@@ -309,22 +369,22 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
     // Depths come in ascending P, so (words per row, small-Dmax / plane
     // count) classes form contiguous runs: dispatch once per run.
     for (int ei = 0; ei < ne;) {
-      const int cls = depth_class(ents[ei]);
+      const int cls = depth_class<(KREG > 0)>(ents[ei]);
       int ej = ei + 1;
-      while (ej < ne && depth_class(ents[ej]) == cls) ++ej;
+      while (ej < ne && depth_class<(KREG > 0)>(ents[ej]) == cls) ++ej;
       const int W = cls >> 5, mode = cls & 31;
       switch (W) {
-        case 1: walk_run<1, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-        case 2: walk_run<2, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-        case 3: walk_run<3, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-        case 4: walk_run<4, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+        case 1: walk_run<1, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+        case 2: walk_run<2, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+        case 3: walk_run<3, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+        case 4: walk_run<4, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
         default:
           if (WMAX > 4) {
             switch (W) {
-              case 5: walk_run<5, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-              case 6: walk_run<6, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-              case 7: walk_run<7, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
-              default: walk_run<8, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base); break;
+              case 5: walk_run<5, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+              case 6: walk_run<6, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+              case 7: walk_run<7, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
+              default: walk_run<8, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
             }
           }
           break;

@@ -134,6 +134,25 @@ def test_exact_branch_counts_vs_oracle():
     p.close()
 
 
+def test_slot_walk_depths_vs_oracle():
+    """9 <= k <= 16 at depths P <= 16 with 10..64 rows take the register slot
+    walk (lp_hist_rows.cu walk_elems), P = 1 included; MC and exact branches,
+    every config, bit-exact counts."""
+    w = resnet152_dp()
+    cases = [(40, 9, False), (100, 12, False), (300, 16, False), (160, 16, False), (64, 13, False),
+             (20, 10, True), (22, 11, True), (30, 12, False)]
+    for n, k, exact in cases:
+        trials = 3000
+        opt = PlannerOptions(mc_trials=trials, exact_cap=1000000 if exact else 0)
+        p = planner(w, opt)
+        cs = [c for c in O.oracle_configs(w, n) if c.stages <= 20]
+        ref, tot = O.oracle_ensemble_counts(n, k, exact, trials, O.planner_seed(0x5EED, n, k), cs)
+        for ci, c in enumerate(cs):
+            got, gt = p.survivor_counts(c, n, k)
+            assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, exact, c)
+        p.close()
+
+
 # ---- phi, plans ---------------------------------------------------------------
 def test_phi_matches_reference():
     for c in load_golden("phi"):
