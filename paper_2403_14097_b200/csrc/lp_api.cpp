@@ -229,9 +229,10 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
 size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int kreg) {
   const size_t nw = (n + 31) / 32;
   const size_t kk = std::max(k, 1);
-  return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(sizeof(DrawConst) * kk) +
-         a16(4 * (size_t)n) + (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) +
-         a16(4 * (nw + 1) * T) + (kreg == 0 ? a16(4 * kk * T) : 0);
+  return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(8 * (size_t)(ne_res + 1)) +
+         a16(sizeof(DrawConst) * kk) + a16(4 * (size_t)n) +
+         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (nw + 1) * T) +
+         (kreg == 0 ? a16(4 * kk * T) : 0);
 }
 
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {

@@ -40,9 +40,23 @@ template <bool SMEM_EVT>
 __device__ __forceinline__ void evt_add(uint32_t* base, int idx) {
   if (SMEM_EVT) {
     const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(base + (idx >> 1)));
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(1u << ((idx & 1) << 4)) : "memory");
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"((idx & 1) * 0xffffu + 1u) : "memory");
   } else {
     atomicAdd(base + idx, 1u);
+  }
+}
+
+// Rows where the running maximum rose, as a bit mask (u32 when Dmax <= 32):
+// the first rise is t = 1 (h0's event), the i-th further one is t = i + 1.
+template <bool SMEM_EVT, typename M>
+__device__ __forceinline__ void emit_rises(M rises, uint32_t* eb, int eo, int Dm) {
+  rises &= rises - 1;
+  while (rises) {
+    const int x = sizeof(M) == 8 ? __ffsll(static_cast<long long>(rises)) - 1
+                                 : __ffs(static_cast<int>(rises)) - 1;
+    rises &= rises - 1;
+    evt_add<SMEM_EVT>(eb, eo + x);
+    eo += Dm;
   }
 }
 
@@ -111,7 +125,7 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
 // a warp-uniform test, every lane walks the same depth), and the rows where
 // the maximum rose are kept as a 64-bit mask, so the row loop has no branch;
 // the events are emitted once after the walk.
-template <int B, bool SMEM_EVT>
+template <int B, bool SMEM_EVT, typename M>
 __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t P, int Dm,
                                            uint32_t* eb, int eoff) {
   uint32_t Dp[B];
@@ -121,7 +135,7 @@ __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t 
   uint32_t w0 = BMc[0], w1 = BMc[T];
   const uint32_t* next = BMc + 2 * T;
   uint32_t sh = 0;
-  unsigned long long rises = 0;
+  M rises = 0;
   for (int x = 0; x < Dm; ++x) {
     const uint32_t R = __funnelshift_r(w0, w1, sh) & tmask;
     uint32_t z = 0;
@@ -129,7 +143,7 @@ __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t 
     for (int l = 0; l < B; ++l) z |= Dp[l];
     const uint32_t hit = R & ~z;
     const uint32_t keep = hit ? 0u : 0xffffffffu;  // all-ones: decrement by R
-    rises |= static_cast<unsigned long long>(hit != 0u) << x;
+    rises |= static_cast<M>(hit != 0u) << x;
     uint32_t c = R ^ (~keep & tmask);
 #pragma unroll
     for (int l = 0; l < B; ++l) {
@@ -145,13 +159,7 @@ __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t 
       next += T;
     }
   }
-  rises &= rises - 1;  // the first rise is t = 1 (h0's event)
-  int t = 2;
-  while (rises) {
-    const int x = __ffsll(rises) - 1;
-    rises &= rises - 1;
-    evt_add<SMEM_EVT>(eb, eoff + (t++ - 2) * Dm + x);
-  }
+  emit_rises<SMEM_EVT>(rises, eb, eoff, Dm);
 }
 
 // Depths with Dmax = DM <= 4 rows: the rows are unrolled at compile time and
@@ -204,10 +212,11 @@ __device__ __forceinline__ void walk_small(const uint32_t* BMc, int T, uint32_t 
 // equals it; the rows where that happened are kept as a mask and the events
 // emitted after the walk, as in walk_rows1.  Branch-free: slots past lim
 // (and the 0xffffffff padding) count nothing.
-template <int KS, bool P1, bool SMEM_EVT>
+template <int KS, bool P1, bool SMEM_EVT, typename M>
 __device__ __forceinline__ void walk_elems(const uint32_t (&s)[KS], uint32_t P, uint32_t magic,
                                            uint32_t lim, int Dm, uint32_t* eb, int eo) {
-  unsigned long long cnt = 0ull, rises = 0ull;
+  unsigned long long cnt = 0ull;
+  M rises = 0;
   uint32_t mx = 0;
   const uint32_t negP = 0u - P;
 #pragma unroll
@@ -218,35 +227,48 @@ __device__ __forceinline__ void walk_elems(const uint32_t (&s)[KS], uint32_t P, 
     const uint32_t c = static_cast<uint32_t>(cnt >> sh) & 15u;
     const bool hit = v < lim && c == mx;
     mx += hit ? 1u : 0u;
-    rises |= static_cast<unsigned long long>(hit) << (q & 63u);
+    rises |= static_cast<M>(hit) << (q & (8u * sizeof(M) - 1u));
     // slots are sorted, so the ones past lim come last: counting them is harmless
     cnt += 1ull << sh;
   }
-  rises &= rises - 1;  // the first rise is t = 1 (h0's event)
-  int t = 2;
-  while (rises) {
-    const int x = __ffsll(rises) - 1;
-    rises &= rises - 1;
-    evt_add<SMEM_EVT>(eb, eo + (t++ - 2) * Dm + x);
-  }
+  emit_rises<SMEM_EVT>(rises, eb, eo, Dm);
 }
 
 template <int W, int B, bool SMEM_EVT>
 __device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P, int Dm,
                                          uint32_t* eb, int eoff) {
-  if (W == 1 && Dm <= 64) walk_rows1<B, SMEM_EVT>(BMc, T, P, Dm, eb, eoff);
+  if (W == 1 && Dm <= 64) walk_rows1<B, SMEM_EVT, unsigned long long>(BMc, T, P, Dm, eb, eoff);
   else walk_rows<W, B, SMEM_EVT>(BMc, T, P, Dm, eb, eoff);
 }
 
-// (words per row, mode): mode = Dmax for Dmax <= 4 (walk_small), 5 for the
-// slot walk (ELEMS: k <= 16 slots in registers; P <= 16 and >= 10 rows),
-// else 8 + plane count (walk_rows).
+// (words per row, mode):
+//   2..4    Dmax <= 4: walk_small
+//   5, 6    slot walk (ELEMS: k <= 16 slots in registers; P <= 16 and 10..64
+//           rows), rise mask u32 / u64
+//   8 + B   walk_rows (walk_rows1 with a u64 rise mask when W = 1, Dmax <= 64)
+//   16 + B  walk_rows1 with a u32 rise mask (W = 1, Dmax <= 32)
+// B = plane count = bits(tmax).
 template <bool ELEMS>
 __device__ __forceinline__ int depth_class(const EntryDesc& e) {
   const int W = (e.P + 31) >> 5;
-  if (ELEMS && e.P <= 16 && e.Dmax >= 10 && e.Dmax <= 64) return (1 << 5) | 5;
-  const int mode = e.Dmax <= 4 ? e.Dmax : 8 + (32 - __clz(static_cast<uint32_t>(e.tmax)));
-  return (W << 5) | mode;
+  if (ELEMS && e.P <= 16 && e.Dmax >= 10 && e.Dmax <= 64) return (1 << 5) | (e.Dmax <= 32 ? 5 : 6);
+  if (e.Dmax <= 4) return (W << 5) | e.Dmax;
+  const int B = 32 - __clz(static_cast<uint32_t>(e.tmax));
+  return (W << 5) | ((W == 1 && e.Dmax <= 32 ? 16 : 8) + B);
+}
+
+template <int KS, bool SMEM_EVT, typename M>
+__device__ __forceinline__ void elems_run(const EntryDesc* ents, int e0, int e1, uint32_t* eb,
+                                          const uint32_t (&sl)[KS]) {
+  for (int e = e0; e < e1; ++e) {
+    const EntryDesc& x = ents[e];
+    const uint32_t P = static_cast<uint32_t>(x.P);
+    if (P == 1u)
+      walk_elems<KS, true, SMEM_EVT, M>(sl, P, 0u, static_cast<uint32_t>(x.lim), x.Dmax, eb, x.evt_off);
+    else
+      walk_elems<KS, false, SMEM_EVT, M>(sl, P, x.magic, static_cast<uint32_t>(x.lim), x.Dmax, eb,
+                                         x.evt_off);
+  }
 }
 
 template <int W, bool SMEM_EVT, int KS>
@@ -261,21 +283,21 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
     CALL;                                                                         \
   }                                                                               \
   return;
+#define LP_R1(B) LP_RUN((walk_rows1<B, SMEM_EVT, uint32_t>(BMc, T, P, Dm, eb, eo)))
+  if (W == 1 && KS > 1 && mode == 5) return elems_run<KS, SMEM_EVT, uint32_t>(ents, e0, e1, eb, sl);
+  if (W == 1 && KS > 1 && mode == 6)
+    return elems_run<KS, SMEM_EVT, unsigned long long>(ents, e0, e1, eb, sl);
+  if (W == 1 && mode > 16) {
+    switch (mode) {
+      case 18: LP_R1(2)
+      case 19: LP_R1(3)
+      case 20: LP_R1(4)
+      case 21: LP_R1(5)
+      case 22: LP_R1(6)
+      default: break;  // tmax <= Dmax <= 32: at most 6 planes
+    }
+  }
   switch (mode) {
-    case 5:
-      if (W == 1 && KS > 1) {
-        for (int e = e0; e < e1; ++e) {
-          const EntryDesc& x = ents[e];
-          const uint32_t P = static_cast<uint32_t>(x.P);
-          if (P == 1u)
-            walk_elems<KS, true, SMEM_EVT>(sl, P, 0u, static_cast<uint32_t>(x.lim), x.Dmax, eb, x.evt_off);
-          else
-            walk_elems<KS, false, SMEM_EVT>(sl, P, x.magic, static_cast<uint32_t>(x.lim), x.Dmax, eb,
-                                            x.evt_off);
-        }
-        return;
-      }
-      break;
     case 2: LP_RUN((walk_small<2, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 3: LP_RUN((walk_small<3, W, SMEM_EVT>(BMc, T, P, eb, eo)))
     case 4: LP_RUN((walk_small<4, W, SMEM_EVT>(BMc, T, P, eb, eo)))
@@ -287,6 +309,7 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
     case 15: LP_RUN((walk_gen<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
     default: LP_RUN((walk_gen<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
   }
+#undef LP_R1
 #undef LP_RUN
 }
 
@@ -315,6 +338,7 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
 
   unsigned char* p = smem;
   EntryDesc* ents = carve<EntryDesc>(p, ne > 0 ? ne : 1);
+  int2* runs = carve<int2>(p, ne + 1);  // (first entry, class) of each class run
   DrawConst* dc = carve<DrawConst>(p, k > 0 ? k : 1);
   uint32_t* h0 = carve<uint32_t>(p, n);
   uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, evt_words) : nullptr;
@@ -331,6 +355,27 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   for (int i = tid; i < n; i += T) h0[i] = 0u;
   for (int i = tid; i < evt_words; i += T) evt[i] = 0u;
   __syncthreads();
+  // Depths come in ascending P, so (words per row, walk mode) classes form
+  // contiguous runs: one warp lists them once per block, and every scenario
+  // dispatches once per run.
+  __shared__ int nruns_s;
+  if (tid < 32) {
+    int cnt = 0;
+    for (int b = 0; b < ne; b += 32) {
+      const int i = b + tid;
+      const int c = i < ne ? depth_class<(KREG > 0)>(ents[i]) : -1;
+      const bool start = i < ne && (i == 0 || depth_class<(KREG > 0)>(ents[i - 1]) != c);
+      const unsigned m = __ballot_sync(0xffffffffu, start);
+      if (start) runs[cnt + __popc(m & ((1u << tid) - 1u))] = make_int2(i, c);
+      cnt += __popc(m);
+    }
+    if (tid == 0) {
+      runs[cnt] = make_int2(ne, 0);
+      nruns_s = cnt;
+    }
+  }
+  __syncthreads();
+  const int nruns = nruns_s;
   uint32_t* evt_base = SMEM_EVT ? evt : evt_g + w.evt_lo;
   uint32_t* BMc = BM + tid;
 
@@ -366,12 +411,9 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
     }
     if (own_h0 && k > 0) atomicAdd(&h0[s0], 1u);
 
-    // Depths come in ascending P, so (words per row, small-Dmax / plane
-    // count) classes form contiguous runs: dispatch once per run.
-    for (int ei = 0; ei < ne;) {
-      const int cls = depth_class<(KREG > 0)>(ents[ei]);
-      int ej = ei + 1;
-      while (ej < ne && depth_class<(KREG > 0)>(ents[ej]) == cls) ++ej;
+    for (int ri = 0; ri < nruns; ++ri) {
+      const int2 r0 = runs[ri];
+      const int ei = r0.x, ej = runs[ri + 1].x, cls = r0.y;
       const int W = cls >> 5, mode = cls & 31;
       switch (W) {
         case 1: walk_run<1, SMEM_EVT>(mode, ents, ei, ej, BMc, T, evt_base, sl); break;
@@ -389,7 +431,6 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
           }
           break;
       }
-      ei = ej;
     }
   }
   __syncthreads();
