@@ -226,13 +226,18 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
         out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
 }
 
-size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int kreg) {
+// Must match the carve in hist_rows_kernel (lp_hist_rows.cu).
+size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int kreg, bool exact) {
   const size_t nw = (n + 31) / 32;
   const size_t kk = std::max(k, 1);
+  size_t gen = 0;  // KREG = 0: displacement list, or position table + displaced bitmap (n <= 256)
+  if (kreg == 0) {
+    gen = 4 * kk * T;
+    if (!exact && n <= 256) gen = std::max(gen, 4 * nw * T + (size_t)((n + 3) & ~3) * T);
+  }
   return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(8 * (size_t)(ne_res + 1)) +
          a16(sizeof(DrawConst) * kk) + a16(4 * (size_t)n) +
-         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (nw + 1) * T) +
-         (kreg == 0 ? a16(4 * kk * T) : 0);
+         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (nw + 1) * T) + a16(gen);
 }
 
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {
@@ -373,8 +378,9 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const int wmax = pmax_res <= 128 ? 4 : 8;
         const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(2 * (size_t)ev) <= kScnFixedBudget;
         int T = 256;
-        while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg) > kSmemBudgetScn) T >>= 1;
-        const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg);
+        while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact) > kSmemBudgetScn)
+          T -= 32;
+        const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};

@@ -155,6 +155,41 @@ __device__ __forceinline__ uint32_t gen_mc_bitmap_smem(uint64_t seed, uint64_t t
   return smin;
 }
 
+// gen_mc_bitmap with the displaced pool positions held in a per-thread byte
+// table (n <= 256, so positions and values fit a byte): TAB[p] is valid when
+// bit p of the thread's displaced bitmap DISc[w * T] is set (the caller
+// zeroes it).  O(1) per draw instead of a scan of the earlier draws.  TAB is
+// this thread's byte column: position p lives in word (p >> 2) * T, byte
+// p & 3, so every lane of a warp stays in its own bank.
+__device__ __forceinline__ uint32_t tab_off(uint32_t p, int T) {
+  return (p & ~3u) * static_cast<uint32_t>(T) + (p & 3u);
+}
+
+__device__ __forceinline__ uint32_t gen_mc_bitmap_tab(uint64_t seed, uint64_t t, int k,
+                                                      const DrawConst* dc, uint8_t* TAB,
+                                                      uint32_t* DISc, uint32_t* BMc, int T) {
+  uint64_t st = trial_state(seed, t);
+  uint32_t smin = 0xffffffffu;
+  for (int i = 0; i < k; ++i) {
+    const uint32_t ui = static_cast<uint32_t>(i);
+    const uint32_t j = ui + draw_below(st, dc[i]);
+    const uint32_t di = DISc[(ui >> 5) * T];
+    uint32_t vi = ui;
+    if ((di >> (ui & 31u)) & 1u) vi = TAB[tab_off(ui, T)];
+    uint32_t* dw = DISc + (j >> 5) * T;
+    const uint32_t dj = *dw;
+    uint32_t vj = j;
+    const uint32_t oj = tab_off(j, T);
+    if ((dj >> (j & 31u)) & 1u) vj = TAB[oj];
+    const uint32_t sel = (j == ui) ? vi : vj;
+    TAB[oj] = static_cast<uint8_t>(vi);  // position j now holds the old pool[i]
+    *dw = dj | (1u << (j & 31u));
+    BMc[(sel >> 5) * T] |= 1u << (sel & 31u);
+    smin = min(smin, sel);
+  }
+  return smin;
+}
+
 // Saturated binomial C(a, b) from the exact pair's table, indexed by
 // (a, min(b, a-b)); callers guarantee a - b <= n - k and b <= k.
 __device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int stride, int a, int b) {

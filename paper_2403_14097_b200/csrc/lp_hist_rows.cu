@@ -343,7 +343,22 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   uint32_t* h0 = carve<uint32_t>(p, n);
   uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, evt_words) : nullptr;
   uint32_t* BM = carve<uint32_t>(p, static_cast<size_t>(nw + 1) * T);  // +1 zero word
-  uint32_t* MAP = (KREG == 0) ? carve<uint32_t>(p, static_cast<size_t>(k > 0 ? k : 1) * T) : nullptr;
+  // KREG = 0 generator scratch (sized as smem_rows in lp_api.cpp): the
+  // displacement list MAP[i * T], or for n <= 256 the displaced bitmap
+  // DIS[w * T] followed by the byte position table.
+  const bool use_tab = KREG == 0 && !pd.exact && n <= 256;
+  uint32_t* MAP = nullptr;
+  uint32_t* DIS = nullptr;
+  uint8_t* TAB = nullptr;
+  if (KREG == 0) {
+    const size_t kk = k > 0 ? k : 1;
+    size_t gen = 4 * kk * T;
+    if (use_tab) gen = max(gen, 4 * static_cast<size_t>(nw) * T + static_cast<size_t>((n + 3) & ~3) * T);
+    unsigned char* g = carve<unsigned char>(p, gen);
+    MAP = reinterpret_cast<uint32_t*>(g);
+    DIS = reinterpret_cast<uint32_t*>(g);
+    TAB = g + 4 * static_cast<size_t>(nw) * T;
+  }
 
   for (int i = tid; i < ne; i += T) {
     EntryDesc e = entries[w.e_lo + i];
@@ -406,6 +421,9 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
         BMc[(c >> 5) * T] |= 1u << (c & 31);
         ++c;
       }
+    } else if (use_tab) {
+      for (int i = 0; i < nw; ++i) DIS[i * T + tid] = 0u;
+      s0 = gen_mc_bitmap_tab(pd.seed, t, k, dc, TAB + 4 * tid, DIS + tid, BMc, T);
     } else {
       s0 = gen_mc_bitmap_smem(pd.seed, t, k, dc, MAP + tid, T, BMc, T);
     }

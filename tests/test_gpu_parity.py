@@ -153,6 +153,24 @@ def test_slot_walk_depths_vs_oracle():
         p.close()
 
 
+def test_table_generator_vs_oracle():
+    """k > 16 at n <= 256 draws through the byte position table
+    (lp_device.cuh gen_mc_bitmap_tab); n > 256 through the displacement list.
+    Every config, bit-exact counts, up to k = n - 1."""
+    w = resnet152_dp()
+    for n, k in [(256, 17), (256, 40), (200, 64), (129, 100), (256, 255), (64, 63), (300, 40), (257, 33)]:
+        trials = 2000
+        opt = PlannerOptions(mc_trials=trials, exact_cap=0)
+        p = planner(w, opt)
+        cs = O.oracle_configs(w, n)
+        cs = cs[:: max(1, len(cs) // 60)]
+        ref, tot = O.oracle_ensemble_counts(n, k, False, trials, O.planner_seed(0x5EED, n, k), cs)
+        for ci, c in enumerate(cs):
+            got, gt = p.survivor_counts(c, n, k)
+            assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, c)
+        p.close()
+
+
 # ---- phi, plans ---------------------------------------------------------------
 def test_phi_matches_reference():
     for c in load_golden("phi"):
