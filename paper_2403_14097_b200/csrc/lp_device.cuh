@@ -27,8 +27,14 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
 }
 
 // Lemire/Kaser/Kurz fastmod: a % d for 32-bit a, d with fm = ceil(2^64 / d).
+// The high product (L * d) >> 64 of L = fm * a mod 2^64 is formed from the
+// 32-bit halves, (hi * d + ((lo * d) >> 32)) >> 32, which is exact: the
+// dropped low word only contributes a fraction below one.
 __device__ __forceinline__ uint32_t fastmod32(uint32_t a, uint64_t fm, uint32_t d) {
-  return static_cast<uint32_t>(__umul64hi(fm * static_cast<uint64_t>(a), static_cast<uint64_t>(d)));
+  const uint64_t L = fm * static_cast<uint64_t>(a);
+  const uint32_t lo = static_cast<uint32_t>(L), hi = static_cast<uint32_t>(L >> 32);
+  const uint64_t t = static_cast<uint64_t>(hi) * d + __umulhi(lo, d);
+  return static_cast<uint32_t>(t >> 32);
 }
 
 // r % b for 64-bit r and b < 2^16: ((hi % b) * (2^32 % b) + lo % b) % b.
