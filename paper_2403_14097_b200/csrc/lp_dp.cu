@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "liveput.h"
 #include "lp_layout.h"
@@ -92,30 +93,65 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
   const double teff_rb = (0.0 < te_rb) ? te_rb : 0.0;
   const bool same_depth = nx.p == pv.p;
   double committed = 0.0, cost_sum = 0.0;
-  for (int d = dmax; d >= 0; --d) {  // m = D - d ascending
-    const double p = prob(d);
-    if (p == 0.0) continue;
-    const int m = pv.d - d;
-    double cost, t_eff;
-    if (m == 0) {
-      cost = c_rb;
-      t_eff = teff_rb;
-    } else if (!same_depth) {
-      cost = c_pipe;
-      t_eff = teff_pipe;
-    } else {
-      bool rb;
-      cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
-      const double te = __dsub_rn(S.T, cost);
-      t_eff = (0.0 < te) ? te : 0.0;
+  if (!same_depth && !S.strict) {
+    // Depth change (most pairs): every bin but m = 0 costs c_pipe at the
+    // next config's own rate.  Empty bins add +0.0 to non-negative sums,
+    // which is exact, so the loop needs no per-bin branch; bins are fetched
+    // eight at a time ahead of the order-fixed accumulation.
+    const double rate = nc.thr;
+    int d = dmax;
+    if (dmax == pv.d) {  // m = 0: rollback
+      const double p = prob(d);
+      committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(p, rate), teff_rb));
+      cost_sum = __dadd_rn(cost_sum, __dmul_rn(p, c_rb));
+      --d;
     }
-    double rate = nc.thr;
-    if (S.strict) {
-      const int alive = min(nx.d, m);
-      rate = alive > 0 ? thr_tab[thr_row[nx.p] + alive] : 0.0;
+    for (int d0 = d; d0 >= 0; d0 -= 8) {
+      double pr[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) pr[u] = (d0 - u >= 0) ? prob(d0 - u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr[u], rate), teff_pipe));
+        cost_sum = __dadd_rn(cost_sum, __dmul_rn(pr[u], c_pipe));
+      }
     }
-    committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(p, rate), t_eff));
-    cost_sum = __dadd_rn(cost_sum, __dmul_rn(p, cost));
+    o.committed = committed;
+    o.mig = cost_sum;
+    return o;
+  }
+  for (int d0 = dmax; d0 >= 0; d0 -= 8) {  // m = D - d ascending
+    double pr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pr[u] = (d0 - u >= 0) ? prob(d0 - u) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int d = d0 - u;
+      if (d < 0) break;
+      const double p = pr[u];
+      if (p == 0.0) continue;
+      const int m = pv.d - d;
+      double cost, t_eff;
+      if (m == 0) {
+        cost = c_rb;
+        t_eff = teff_rb;
+      } else if (!same_depth) {
+        cost = c_pipe;
+        t_eff = teff_pipe;
+      } else {
+        bool rb;
+        cost = transition_cost(m, pv.d, pv.p, nx.d, nx.p, L.fixed, nc, S, &rb);
+        const double te = __dsub_rn(S.T, cost);
+        t_eff = (0.0 < te) ? te : 0.0;
+      }
+      double rate = nc.thr;
+      if (S.strict) {
+        const int alive = min(nx.d, m);
+        rate = alive > 0 ? thr_tab[thr_row[nx.p] + alive] : 0.0;
+      }
+      committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(p, rate), t_eff));
+      cost_sum = __dadd_rn(cost_sum, __dmul_rn(p, cost));
+    }
   }
   o.committed = committed;
   o.mig = cost_sum;
@@ -357,7 +393,12 @@ cudaError_t launch_dp_step(int j, int next_count, int prev_count, cudaStream_t s
   if (blocks <= 0) return cudaSuccess;
   // 128 threads per next node measured fastest (more threads per node cost
   // more in the cross-warp reduction than the shorter phi chains save)
-  const int threads = std::min(128, std::max(32, (prev_count + 31) / 32 * 32));
+  static const int cap = [] {
+    const char* e = getenv("LIVEPUT_DP_THREADS");
+    const int v = e ? atoi(e) : 0;
+    return (v >= 32 && v <= 512) ? v : 128;
+  }();
+  const int threads = std::min(cap, std::max(32, (prev_count + 31) / 32 * 32));
   dp_step_kernel<<<blocks, threads, 0, st>>>(j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val,
                                              mig, parent, stc, stm);
   return cudaGetLastError();
