@@ -716,7 +716,10 @@ struct lp_handle {
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
-         w_plan = 0, w_live = 0, w_final = 0;
+         w_plan = 0, w_live = 0, w_final = 0, w_bar = 0;
+  int max_next = 0;         // largest level (next role), for the persistent DP grid
+  bool live_pending = false;  // liveput rows of the last execute not yet computed
+  bool dp_launches = false;  // LIVEPUT_DP=launches: one kernel per level (A/B)
   DevBuf tables, work;
   PinBuf pin_up, pin_down;
   size_t up_bytes = 0;
@@ -724,6 +727,7 @@ struct lp_handle {
   // DP tables: a second image, so lp_replan can build and upload them while
   // the histogram kernels run
   DevBuf tables2;
+  DevBuf dp_trace;  // LIVEPUT_DP_TRACE
   PinBuf pin_up2;
   cudaEvent_t ev_up[2] = {nullptr, nullptr};  // last upload out of pin_up / pin_up2
   struct PrepState {
@@ -974,6 +978,10 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   for (auto& ev : h->ev_up) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  {
+    const char* e = getenv("LIVEPUT_DP");
+    h->dp_launches = (e && std::string(e) == "launches");
+  }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = h;
   return LP_OK;
@@ -1239,6 +1247,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->w_plan = take(sizeof(lp_plan_step) * H);
   h->w_live = take(sizeof(lp_liveput_row) * std::max<size_t>(nn, 1));  // >= liveput rows
   h->w_final = take(8);
+  h->w_bar = take(4);
   LP_CUDA(h, h->work.ensure(o));
   mark("upload1");
   std::memset(&h->stats, 0, sizeof h->stats);
@@ -1343,6 +1352,8 @@ lp_status prepare_dp(lp_handle* h) {
   }
   h->S = dp_scalars(h, H);
   mark("lrows");
+  h->max_next = 0;
+  for (const LevelDesc& L : h->levels) h->max_next = std::max(h->max_next, L.next_count);
   size_t bytes = 0;
   lp_status us = upload_image(h,
                               {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
@@ -1383,10 +1394,13 @@ lp_status exec_hist(lp_handle* h) {
     if (r != ncclSuccess) return fail(h, LP_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(r));
   }
   LP_CUDA(h, cudaEventRecord(h->ev[2], st));
-  LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
-                              dptr<int32_t>(h->tables, h->off_store_off),
-                              static_cast<double*>(h->store.p)));
-  h->stats.kernel_launches = launches + 1;
+  if (h->dp_launches) {
+    LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
+                                dptr<int32_t>(h->tables, h->off_store_off),
+                                static_cast<double*>(h->store.p)));
+    ++launches;
+  }
+  h->stats.kernel_launches = launches;
   return LP_OK;
 }
 
@@ -1405,6 +1419,38 @@ lp_status exec_dp(lp_handle* h) {
   double* stc = dptr<double>(h->work, h->w_stc);
   double* stm = dptr<double>(h->work, h->w_stm);
   double* histp = static_cast<double*>(h->store.p);
+  if (!h->dp_launches && h->horizon <= kMaxHorizon) {
+    DpArgs a{};
+    a.levels = lv;
+    a.cfg = cfg;
+    a.pcost = pcost;
+    a.thr_tab = thr;
+    a.thr_row = throw_;
+    a.pairs = dptr<PairDesc>(h->tables, h->off_pairs);
+    a.entries = dptr<EntryDesc>(h->tables, h->off_entries);
+    a.hist = dptr<uint32_t>(h->work, h->w_hist);
+    a.store_off = dptr<int32_t>(h->tables, h->off_store_off);
+    a.n_entries = (int)h->hp.entries.size();
+    a.store = histp;
+    a.val = val;
+    a.mig = mig;
+    a.parent = par;
+    a.stc = stc;
+    a.stm = stm;
+    a.plan = dptr<lp_plan_step>(h->work, h->w_plan);
+    a.final_value = dptr<double>(h->work, h->w_final);
+    a.barrier = dptr<uint32_t>(h->work, h->w_bar);
+    a.horizon = h->horizon;
+    static const bool trace = getenv("LIVEPUT_DP_TRACE") != nullptr;
+    if (trace) {
+      const size_t nb = (size_t)h->num_sms * 8 * (2 * kTraceLevels + 2);
+      LP_CUDA(h, h->dp_trace.ensure(nb * 8));
+      LP_CUDA(h, cudaMemsetAsync(h->dp_trace.p, 0, nb * 8, st));
+      a.trace = static_cast<uint64_t*>(h->dp_trace.p);
+    }
+    LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S));
+    ++launches;
+  } else {
   LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
   LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
   for (int j = 0; j < h->horizon; ++j) {
@@ -1416,14 +1462,25 @@ lp_status exec_dp(lp_handle* h) {
                              dptr<lp_plan_step>(h->work, h->w_plan),
                              dptr<double>(h->work, h->w_final)));
   ++launches;
-  if (!h->lrows.empty()) {
-    LP_CUDA(h, launch_liveput((int)h->lrows.size(), st, dptr<int4>(h->tables2, h->off_lrows), lv,
-                              cfg, nullptr, histp, thr, throw_,
-                              dptr<lp_liveput_row>(h->work, h->w_live)));
-    ++launches;
   }
   LP_CUDA(h, cudaEventRecord(h->ev[3], st));
+  h->live_pending = !h->lrows.empty();  // the liveput table is built on demand (lp_fetch)
   h->stats.kernel_launches += launches;
+  return LP_OK;
+}
+
+// Liveput table rows of the last execute, Σ_m p_m·thr(m, P) per (interval,
+// prev config); launched only when a caller asks for them.
+lp_status exec_liveput(lp_handle* h) {
+  if (!h->live_pending) return LP_OK;
+  LP_CUDA(h, launch_liveput((int)h->lrows.size(), h->stream, dptr<int4>(h->tables2, h->off_lrows),
+                            dptr<LevelDesc>(h->tables2, h->off_levels),
+                            dptr<NodeCfg>(h->tables2, h->off_cfg), nullptr,
+                            static_cast<double*>(h->store.p), dptr<double>(h->tables2, h->off_thr),
+                            dptr<int32_t>(h->tables2, h->off_throw),
+                            dptr<lp_liveput_row>(h->work, h->w_live)));
+  h->live_pending = false;
+  ++h->stats.kernel_launches;
   return LP_OK;
 }
 
@@ -1452,6 +1509,10 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_
   const size_t plan_b = sizeof(lp_plan_step) * h->horizon;
   const size_t nl = live ? std::min<size_t>(h->lrows.size(), (size_t)std::max(cap, 0)) : 0;
   const size_t live_b = sizeof(lp_liveput_row) * nl;
+  if (live_b) {
+    lp_status ls = exec_liveput(h);
+    if (ls != LP_OK) return ls;
+  }
   LP_CUDA(h, h->pin_down.ensure(plan_b + live_b + 64));
   unsigned char* pd = static_cast<unsigned char*>(h->pin_down.p);
   LP_CUDA(h, cudaMemcpyAsync(pd, dptr<void>(h->work, h->w_plan), plan_b, cudaMemcpyDeviceToHost,
@@ -1460,6 +1521,40 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_
     LP_CUDA(h, cudaMemcpyAsync(pd + plan_b, dptr<void>(h->work, h->w_live), live_b,
                                cudaMemcpyDeviceToHost, h->stream));
   LP_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (h->dp_trace.p && getenv("LIVEPUT_DP_TRACE")) {  // debug: per-level block timing
+    const int per = 2 * kTraceLevels + 2;
+    const size_t nb = (size_t)h->num_sms * 8;
+    std::vector<uint64_t> tr(nb * per);
+    cudaMemcpy(tr.data(), h->dp_trace.p, tr.size() * 8, cudaMemcpyDeviceToHost);
+    int used = 0;
+    while ((size_t)used < nb && tr[(size_t)used * per] != 0) ++used;
+    for (int j = 1; j < std::min(h->horizon, kTraceLevels); ++j) {
+      uint64_t smin = UINT64_MAX, emax = 0;
+      std::vector<double> comp;
+      for (int b = 0; b < used; ++b) {
+        const uint64_t s0 = tr[(size_t)b * per + 3 + 2 * (j - 1)], c = tr[(size_t)b * per + 2 + 2 * j],
+                       e = tr[(size_t)b * per + 3 + 2 * j];
+        smin = std::min(smin, s0);
+        emax = std::max(emax, e);
+        comp.push_back((double)(c - s0) * 1e-3);
+      }
+      std::vector<std::pair<double, int>> bycomp;
+      for (int b = 0; b < used; ++b) bycomp.push_back({comp[b], b});
+      std::sort(comp.begin(), comp.end());
+      std::sort(bycomp.rbegin(), bycomp.rend());
+      fprintf(stderr, "[dp] level %2d: %7.2f us; block compute median %6.2f max %6.2f us (%d blocks) slowest:", j,
+              (double)(emax - smin) * 1e-3, comp[comp.size() / 2], comp.back(), used);
+      const LevelDesc& L = h->levels[j];
+      for (int q = 0; q < 6 && q < (int)bycomp.size(); ++q) {
+        const int b = bycomp[q].second;
+        if (b < L.next_count) {
+          const NodeCfg& c = h->cfg[L.next_base + b];
+          fprintf(stderr, " (%d,%d)%.1f", c.d, c.p, bycomp[q].first);
+        }
+      }
+      fprintf(stderr, "  fastest: (%d)%.1f\n", bycomp.back().second, bycomp.back().first);
+    }
+  }
   std::memcpy(out, pd, plan_b);
   if (live_b) std::memcpy(live, pd + plan_b, live_b);
   if (rows) *rows = (int32_t)h->lrows.size();

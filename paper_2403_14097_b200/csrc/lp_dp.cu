@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "liveput.h"
+#include "lp_launch.h"
 #include "lp_layout.h"
 
 namespace lp {
@@ -68,11 +69,53 @@ __device__ __forceinline__ double transition_cost(int m, int sd, int sp, int td,
 // (rows d = 0..min(k, D), m = D - d).  prob(d) returns hist[m] of the
 // reference, count_m / count (0.0 for an empty bin).  thr_tab/thr_row:
 // throughput(D, P).
+// Bin accessors: probability of bin d, and eight bins d0, d0-1, ... d0-7
+// (0.0 below d = 0) fetched together.
+struct ProbPtr {
+  const double* hp;
+  __device__ __forceinline__ double operator()(int d) const { return hp[d]; }
+  __device__ __forceinline__ void chunk(int d0, double (&pr)[8]) const {
+    const double* q = hp + d0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pr[u] = (u <= d0) ? q[-u] : 0.0;
+  }
+};
+
+struct ProbCounts {  // count_m / count straight from the u32 histogram
+  const uint32_t* h;
+  double total;
+  __device__ __forceinline__ double operator()(int d) const {
+    return h[d] ? __ddiv_rn(static_cast<double>(h[d]), total) : 0.0;
+  }
+  __device__ __forceinline__ void chunk(int d0, double (&pr)[8]) const {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pr[u] = (u <= d0) ? (*this)(d0 - u) : 0.0;
+  }
+};
+
+// Terms of phi that depend only on the level and the next config, in the
+// reference's order: the repartition cost (rollback when m == 0, or any
+// depth change) is ((fixed + build) + update) + pipe (+ rollback penalty).
+struct PhiConst {
+  double base, c_pipe, c_rb, teff_pipe, teff_rb;
+};
+
+__device__ __forceinline__ PhiConst phi_const(const LevelDesc& L, const DpScalars& S, const NodeCost& nc) {
+  PhiConst c;
+  c.base = __dadd_rn(__dadd_rn(L.fixed, S.build), S.update);
+  c.c_pipe = __dadd_rn(c.base, nc.pipe);
+  c.c_rb = __dadd_rn(c.c_pipe, S.rollback);
+  const double te_pipe = __dsub_rn(S.T, c.c_pipe), te_rb = __dsub_rn(S.T, c.c_rb);
+  c.teff_pipe = (0.0 < te_pipe) ? te_pipe : 0.0;
+  c.teff_rb = (0.0 < te_rb) ? te_rb : 0.0;
+  return c;
+}
+
 template <class Prob>
 __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, const NodeCost& nc,
                                           const LevelDesc& L, const DpScalars& S, Prob prob,
                                           const double* __restrict__ thr_tab,
-                                          const int32_t* __restrict__ thr_row) {
+                                          const int32_t* __restrict__ thr_row, const PhiConst& K) {
   PhiOut o{0.0, 0.0};
   if (nx.d <= 0) return o;  // suspended next: nothing committed, nothing moved
   if (pv.d <= 0) {          // resume from suspension (optimizer.cpp:108-115)
@@ -82,15 +125,8 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     return o;
   }
   const int dmax = min(L.k, pv.d);
-  // Terms that do not depend on m, computed once in the reference's order:
-  // the repartition cost (rollback when m == 0, or any depth change) is
-  // ((fixed + build) + update) + pipe (+ rollback penalty).
-  const double base = __dadd_rn(__dadd_rn(L.fixed, S.build), S.update);
-  const double c_pipe = __dadd_rn(base, nc.pipe);
-  const double c_rb = __dadd_rn(c_pipe, S.rollback);
-  const double te_pipe = __dsub_rn(S.T, c_pipe), te_rb = __dsub_rn(S.T, c_rb);
-  const double teff_pipe = (0.0 < te_pipe) ? te_pipe : 0.0;
-  const double teff_rb = (0.0 < te_rb) ? te_rb : 0.0;
+  const double base = K.base, c_pipe = K.c_pipe, c_rb = K.c_rb;
+  const double teff_pipe = K.teff_pipe, teff_rb = K.teff_rb;
   const bool same_depth = nx.p == pv.p;
   double committed = 0.0, cost_sum = 0.0;
   if (!same_depth && !S.strict) {
@@ -108,8 +144,7 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     }
     for (int d0 = d; d0 >= 0; d0 -= 8) {
       double pr[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) pr[u] = (d0 - u >= 0) ? prob(d0 - u) : 0.0;
+      prob.chunk(d0, pr);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr[u], rate), teff_pipe));
@@ -120,10 +155,43 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     o.mig = cost_sum;
     return o;
   }
+  if (!S.strict) {
+    // Same depth: transition_cost per bin, branch-free.  rounds = the least
+    // r with m * 2^r >= max(td, m) (replication_rounds) from the bit lengths;
+    // every FP64 value is computed as the branchy code would and selected.
+    const int sd = pv.d, td = nx.d;
+    const double rate = nc.thr;
+    for (int d0 = dmax; d0 >= 0; d0 -= 8) {
+      double pr[8];
+      prob.chunk(d0, pr);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int m = sd - (d0 - u);  // bins past d = 0 carry p = 0
+        const int mm = m > 0 ? m : 1;
+        int r = 0;
+        if (td > mm) {
+          r = __clz(mm) - __clz(td);
+          r += ((mm << r) < td) ? 1 : 0;
+        }
+        const double inter_a = __dmul_rn(static_cast<double>(r), nc.unit);
+        const double inter = (nc.pipe < inter_a) ? nc.pipe : inter_a;
+        const double c_rep = __dadd_rn(base, inter);
+        double cost = (r == 0) ? ((m >= sd && td == sd) ? 0.0 : base) : c_rep;
+        cost = (m == 0) ? c_rb : cost;
+        const double te = __dsub_rn(S.T, cost);
+        double t_eff = (0.0 < te) ? te : 0.0;
+        t_eff = (m == 0) ? teff_rb : t_eff;
+        committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr[u], rate), t_eff));
+        cost_sum = __dadd_rn(cost_sum, __dmul_rn(pr[u], cost));
+      }
+    }
+    o.committed = committed;
+    o.mig = cost_sum;
+    return o;
+  }
   for (int d0 = dmax; d0 >= 0; d0 -= 8) {  // m = D - d ascending
     double pr[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) pr[u] = (d0 - u >= 0) ? prob(d0 - u) : 0.0;
+    prob.chunk(d0, pr);
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int d = d0 - u;
@@ -230,12 +298,13 @@ __global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __
     nc.unit = pc.y;
     nc.resume = pc.z;
   }
+  const PhiConst K = phi_const(L, S, nc);
   Cand best{0.0, 0.0, 0.0, 0.0, -1};
   for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
     const int gi = L.prev_base + pi;
     const NodeCfg pv = cfg[gi];
     const double* hp = histp + pv.hist_off;
-    const PhiOut ph = phi_dev(pv, nx, nc, L, S, [hp](int d) { return hp[d]; }, thr_tab, thr_row);
+    const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{hp}, thr_tab, thr_row, K);
     const double v = __dadd_rn(val[gi], ph.committed);
     const double mg = __dadd_rn(mig[gi], ph.mig);
     if (best.idx < 0 || v > best.value || (v == best.value && mg < best.mig)) {
@@ -375,10 +444,7 @@ __global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc
                                   const int32_t* __restrict__ thr_row, double* __restrict__ out2) {
   const double total = static_cast<double>(L.total);
   const uint32_t* h = hist + pv.hist_off;
-  const PhiOut o = phi_dev(
-      pv, nx, nc, L, S,
-      [h, total](int d) { return h[d] ? __ddiv_rn(static_cast<double>(h[d]), total) : 0.0; },
-      thr_tab, thr_row);
+  const PhiOut o = phi_dev(pv, nx, nc, L, S, ProbCounts{h, total}, thr_tab, thr_row, phi_const(L, S, nc));
   out2[0] = o.committed;
   out2[1] = o.mig;
 }
@@ -436,6 +502,214 @@ cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCo
                               cudaStream_t st) {
   phi_single_kernel<<<1, 1, 0, st>>>(pv, nx, nc, L, S, hist, thr_tab, thr_row, out2);
   return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent DP: normalisation, the H level steps, the final pick and the
+// traceback in ONE cooperative launch, separated by a grid barrier instead of
+// H + 2 kernel boundaries.  Values written inside the launch (probabilities,
+// val/mig/parent/step terms) are read back through L2 (ld.cg) or after a
+// barrier that follows their only writes, never through the read-only path.
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Monotone arrival counter (zeroed before the launch): barrier e completes
+// when e * gridDim.x blocks have arrived.
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0) {
+    const uint32_t target = epoch * gridDim.x;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_relaxed_u32(ctr) < target) __nanosleep(20);
+    __threadfence();  // acquire: orders the block's later reads after the arrivals
+  }
+  __syncthreads();
+}
+
+
+__global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScalars S) {
+  __shared__ Cand s_best[8];
+  __shared__ int s_idx[256];
+  __shared__ int s_path[kMaxHorizon + 1];
+  uint32_t epoch = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto stamp = [&](int slot) {  // LIVEPUT_DP_TRACE: per-block globaltimer stamps
+    if (a.trace && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      a.trace[(size_t)blockIdx.x * (2 * kTraceLevels + 2) + slot] = t;
+    }
+  };
+  stamp(0);
+
+  // phase 0: probabilities of the fresh entries
+  for (int e = blockIdx.x; e < a.n_entries; e += gridDim.x) {
+    const EntryDesc en = a.entries[e];
+    const PairDesc pd = a.pairs[en.pair];
+    const int len = hist_row(en.Dmax + 1, pd.k);
+    const double total = static_cast<double>(pd.count);
+    double* out = a.store + a.store_off[e];
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint32_t c = a.hist[en.hist_off + i];
+      out[i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    a.val[0] = 0.0;  // level 0: value 0, migration 0
+    a.mig[0] = 0.0;
+  }
+  stamp(1);
+  grid_barrier(a.barrier, epoch);
+
+  // phases 1..H: F_{j+1}[c'] = max_c F_j[c] + phi(c, c'), one block per next node
+  const double* histp = a.store;
+  for (int j = 0; j < a.horizon; ++j) {
+    const LevelDesc L = a.levels[j];
+    for (int nb = blockIdx.x; nb < L.next_count; nb += gridDim.x) {
+      const int ni = L.next_base + nb;
+      const NodeCfg nx = a.cfg[ni];
+      NodeCost nc{0.0, 0.0, 0.0, 0.0};
+      if (nx.d > 0) {
+        const double4 pc = a.pcost[nx.p];
+        nc.thr = a.thr_tab[a.thr_row[nx.p] + nx.d];
+        nc.pipe = pc.x;
+        nc.unit = pc.y;
+        nc.resume = pc.z;
+      }
+      const PhiConst K = phi_const(L, S, nc);
+      Cand best{0.0, 0.0, 0.0, 0.0, -1};
+      // Prev nodes come in ascending P, descending D, so their bin counts
+      // fall along the list: threads take them in snake order (t, 2T-1-t,
+      // 2T+t, ...) to even out the per-thread work; ties are broken on the
+      // index explicitly, so the visiting order does not matter.
+      const int T2 = 2 * static_cast<int>(blockDim.x);
+      for (int r = 0;; ++r) {
+        const int pi = (r & 1) ? (r + 1) * static_cast<int>(blockDim.x) - 1 - static_cast<int>(threadIdx.x)
+                               : r * static_cast<int>(blockDim.x) + static_cast<int>(threadIdx.x);
+        if (r * static_cast<int>(blockDim.x) >= L.prev_count) break;
+        if (pi >= L.prev_count) continue;
+        (void)T2;
+        const int gi = L.prev_base + pi;
+        const NodeCfg pv = a.cfg[gi];
+        const double* hp = histp + pv.hist_off;
+        const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{hp}, a.thr_tab, a.thr_row, K);
+        const double v = __dadd_rn(__ldcg(a.val + gi), ph.committed);
+        const double mg = __dadd_rn(__ldcg(a.mig + gi), ph.mig);
+        if (best.idx < 0 || v > best.value ||
+            (v == best.value && (mg < best.mig || (mg == best.mig && pi < best.idx)))) {
+          best.value = v;
+          best.mig = mg;
+          best.stc = ph.committed;
+          best.stm = ph.mig;
+          best.idx = pi;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const Cand o = shfl_cand(best, lane ^ off);
+        if (cand_better(o, best)) best = o;
+      }
+      if (lane == 0) s_best[warp] = best;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+          if (cand_better(s_best[w], best)) best = s_best[w];
+        __stcg(a.val + ni, best.value);
+        __stcg(a.mig + ni, best.mig);
+        __stcg(a.parent + ni, best.idx);
+        __stcg(a.stc + ni, best.stc);
+        __stcg(a.stm + ni, best.stm);
+      }
+      __syncthreads();
+    }
+    if (j < kTraceLevels) stamp(2 + 2 * j);
+    grid_barrier(a.barrier, epoch);
+    if (j < kTraceLevels) stamp(3 + 2 * j);
+  }
+
+  // final pick (rank = (value, -mig, D, -P), suspended as (-1, 0), first
+  // index wins) and traceback, by block 0
+  if (blockIdx.x != 0) return;
+  const LevelDesc last = a.levels[a.horizon - 1];
+  const int base = last.next_base, cnt = last.next_count;
+  auto gt = [&](int x, int y) -> bool {  // rank(x) > rank(y)
+    if (y < 0) return x >= 0;
+    if (x < 0) return false;
+    const double va = __ldcg(a.val + base + x), vb = __ldcg(a.val + base + y);
+    if (vb < va) return true;
+    if (va < vb) return false;
+    const double ma = -__ldcg(a.mig + base + x), mb = -__ldcg(a.mig + base + y);
+    if (mb < ma) return true;
+    if (ma < mb) return false;
+    const NodeCfg ca = a.cfg[base + x], cb = a.cfg[base + y];
+    const int da = ca.d > 0 ? ca.d : -1, db = cb.d > 0 ? cb.d : -1;
+    if (db < da) return true;
+    if (da < db) return false;
+    const int pa = ca.d > 0 ? -ca.p : 0, pb = cb.d > 0 ? -cb.p : 0;
+    return pb < pa;
+  };
+  int mine = -1;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    if (gt(i, mine)) mine = i;  // ascending i: strict > keeps the first
+  s_idx[threadIdx.x] = mine;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      const int x = s_idx[threadIdx.x], y = s_idx[threadIdx.x + st];
+      if (gt(y, x) || (y >= 0 && x >= 0 && !gt(x, y) && y < x)) s_idx[threadIdx.x] = y;
+    }
+    __syncthreads();
+  }
+  // back-pointer chase: only the parent loads are serial; the plan rows are
+  // then written by one thread per interval
+  if (threadIdx.x == 0) {
+    int idx = s_idx[0];
+    if (a.final_value) *a.final_value = __ldcg(a.val + base + idx);
+    for (int jj = a.horizon; jj >= 1; --jj) {
+      const int gi = a.levels[jj - 1].next_base + idx;
+      s_path[jj] = gi;
+      idx = __ldcg(a.parent + gi);
+    }
+  }
+  __syncthreads();
+  for (int jj = 1 + threadIdx.x; jj <= a.horizon; jj += blockDim.x) {
+    const int gi = s_path[jj];
+    const NodeCfg c = a.cfg[gi];
+    lp_plan_step st;
+    st.interval_index = jj;
+    st.config.pipelines = c.d > 0 ? c.d : 0;
+    st.config.stages = c.d > 0 ? c.p : 0;
+    st.expected_committed = __ldcg(a.stc + gi);
+    st.expected_mig_cost_s = __ldcg(a.stm + gi);
+    a.plan[jj - 1] = st;
+  }
+}
+
+cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStream_t st,
+                                 const DpArgs& a, const DpScalars& S) {
+  if (a.horizon > kMaxHorizon) return cudaErrorInvalidValue;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_persistent_kernel, 256, 0);
+    if (e != cudaSuccess) return e;
+  }
+  (void)device;
+  const int cap = std::max(1, per_sm) * num_sms;
+  const int grid = std::max(1, std::min(cap, std::max(max_next, a.n_entries)));
+  cudaError_t e = cudaMemsetAsync(a.barrier, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  DpArgs aa = a;
+  DpScalars ss = S;
+  void* params[] = {&aa, &ss};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp_persistent_kernel), dim3(grid),
+                                     dim3(256), params, 0, st);
 }
 
 }  // namespace lp

@@ -55,4 +55,36 @@ cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCo
                               const double* thr_tab, const int32_t* thr_row, double* out2,
                               cudaStream_t st);
 
+// Persistent DP (lp_dp.cu): normalisation, every level step, the final pick
+// and the traceback in one cooperative launch.
+struct DpArgs {
+  const LevelDesc* levels;
+  const NodeCfg* cfg;
+  const double4* pcost;
+  const double* thr_tab;
+  const int32_t* thr_row;
+  // normalisation (count / total into the probability store)
+  const PairDesc* pairs;
+  const EntryDesc* entries;
+  const uint32_t* hist;
+  const int32_t* store_off;
+  int n_entries;
+  double* store;
+  // DP state
+  double* val;
+  double* mig;
+  int32_t* parent;
+  double* stc;
+  double* stm;
+  lp_plan_step* plan;
+  double* final_value;
+  uint32_t* barrier;
+  int horizon;
+  uint64_t* trace;  // optional: per block, 2 * kTraceLevels + 2 globaltimer stamps
+};
+constexpr int kTraceLevels = 32;
+
+cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStream_t st,
+                                 const DpArgs& a, const DpScalars& S);
+
 }  // namespace lp

@@ -104,6 +104,8 @@ struct LevelDesc {
   double fixed;                    // fresh > 0 ? fresh_fixed : 0.0
 };
 
+constexpr int kMaxHorizon = 1024;  // persistent DP's traceback buffer
+
 struct DpScalars {
   double T;
   double build, update;
