@@ -237,7 +237,7 @@ size_t smem_rows(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T
   }
   return a16(sizeof(EntryDesc) * std::max(ne_res, 1)) + a16(8 * (size_t)(ne_res + 1)) +
          a16(sizeof(DrawConst) * kk) + a16(4 * (size_t)n) +
-         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (nw + 1) * T) + a16(gen);
+         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (nw + 3) * T) + a16(gen);
 }
 
 size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T, int uw) {

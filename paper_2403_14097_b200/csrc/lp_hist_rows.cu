@@ -234,6 +234,67 @@ __device__ __forceinline__ void walk_elems(const uint32_t (&s)[KS], uint32_t P, 
   emit_rises<SMEM_EVT>(rises, eb, eo, Dm);
 }
 
+// Depths with exactly two rows (P in (n/3, n/2]) for all P of a run at once:
+// (2, x = 1) is the only event, and it happens at P exactly when some slot
+// a < P has a + P selected.  For every selected a below the run's largest P,
+// the bitmap shifted right by a + Plo gives "a + P selected" for all P of the
+// run in one window of WW words (P <= a masked off); the OR over a marks the
+// depths with an event.  Cost ~ (slots below Phi) * WW instead of
+// (depths) * 2 rows * ceil(P/32).
+template <int WW, bool SMEM_EVT>
+__device__ __forceinline__ void dm2_run(const EntryDesc* ents, int e0, int e1, const uint32_t* BMc,
+                                        int T, uint32_t* eb) {
+  const int Plo = ents[e0].P, Phi = ents[e1 - 1].P;
+  uint32_t E[WW];
+#pragma unroll
+  for (int i = 0; i < WW; ++i) E[i] = 0u;
+  const int wlast = (Phi - 1) >> 5;
+  for (int w = 0; w <= wlast; ++w) {
+    uint32_t bits = BMc[w * T];
+    if (w == wlast) {
+      const int top = (Phi - 1) & 31;  // keep a <= Phi - 1
+      bits &= top == 31 ? 0xffffffffu : ((2u << top) - 1u);
+    }
+    while (bits) {
+      const int a = w * 32 + __ffs(static_cast<int>(bits)) - 1;
+      bits &= bits - 1;
+      const uint32_t sbit = static_cast<uint32_t>(a + Plo);
+      const uint32_t* src = BMc + (sbit >> 5) * T;
+      const uint32_t sh = sbit & 31u;
+      const int cut = a - Plo + 1;  // window bits b < cut have P <= a
+      uint32_t lo = src[0];
+#pragma unroll
+      for (int i = 0; i < WW; ++i) {
+        const uint32_t hi = src[(i + 1) * T];
+        const uint32_t x = __funnelshift_r(lo, hi, sh);
+        lo = hi;
+        const int rel = cut - 32 * i;
+        const uint32_t keep = rel <= 0 ? 0xffffffffu : (rel >= 32 ? 0u : (0xffffffffu << rel));
+        E[i] |= x & keep;
+      }
+    }
+  }
+  const int width = Phi - Plo + 1;
+  if (Phi - Plo == e1 - e0 - 1) {  // one entry per P of the run
+#pragma unroll
+    for (int i = 0; i < WW; ++i) {
+      const int rel = width - 32 * i;
+      uint32_t bits = E[i] & (rel >= 32 ? 0xffffffffu : (rel <= 0 ? 0u : ((1u << rel) - 1u)));
+      while (bits) {
+        const int b = 32 * i + __ffs(static_cast<int>(bits)) - 1;
+        bits &= bits - 1;
+        evt_add<SMEM_EVT>(eb, ents[e0 + b].evt_off + 1);
+      }
+    }
+  } else {
+    for (int e = e0; e < e1; ++e) {
+      const int b = ents[e].P - Plo;
+      const uint32_t wv = WW == 1 ? E[0] : (b < 32 ? E[0] : (WW == 2 || b < 64 ? E[WW > 1 ? 1 : 0] : E[WW - 1]));
+      if ((wv >> (b & 31)) & 1u) evt_add<SMEM_EVT>(eb, ents[e].evt_off + 1);
+    }
+  }
+}
+
 template <int W, int B, bool SMEM_EVT>
 __device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P, int Dm,
                                          uint32_t* eb, int eoff) {
@@ -252,6 +313,7 @@ template <bool ELEMS>
 __device__ __forceinline__ int depth_class(const EntryDesc& e) {
   const int W = (e.P + 31) >> 5;
   if (ELEMS && e.P <= 16 && e.Dmax >= 10 && e.Dmax <= 64) return (1 << 5) | (e.Dmax <= 32 ? 5 : 6);
+  if (e.Dmax == 2) return (1 << 5) | 7;  // all two-row depths: dm2_run
   if (e.Dmax <= 4) return (W << 5) | e.Dmax;
   const int B = 32 - __clz(static_cast<uint32_t>(e.tmax));
   return (W << 5) | ((W == 1 && e.Dmax <= 32 ? 16 : 8) + B);
@@ -284,6 +346,12 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
   }                                                                               \
   return;
 #define LP_R1(B) LP_RUN((walk_rows1<B, SMEM_EVT, uint32_t>(BMc, T, P, Dm, eb, eo)))
+  if (W == 1 && mode == 7) {
+    const int ww = ((ents[e1 - 1].P - ents[e0].P) >> 5) + 1;
+    if (ww == 1) return dm2_run<1, SMEM_EVT>(ents, e0, e1, BMc, T, eb);
+    if (ww == 2) return dm2_run<2, SMEM_EVT>(ents, e0, e1, BMc, T, eb);
+    return dm2_run<3, SMEM_EVT>(ents, e0, e1, BMc, T, eb);
+  }
   if (W == 1 && KS > 1 && mode == 5) return elems_run<KS, SMEM_EVT, uint32_t>(ents, e0, e1, eb, sl);
   if (W == 1 && KS > 1 && mode == 6)
     return elems_run<KS, SMEM_EVT, unsigned long long>(ents, e0, e1, eb, sl);
@@ -342,7 +410,7 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   DrawConst* dc = carve<DrawConst>(p, k > 0 ? k : 1);
   uint32_t* h0 = carve<uint32_t>(p, n);
   uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, evt_words) : nullptr;
-  uint32_t* BM = carve<uint32_t>(p, static_cast<size_t>(nw + 1) * T);  // +1 zero word
+  uint32_t* BM = carve<uint32_t>(p, static_cast<size_t>(nw + 3) * T);  // +3 zero words (dm2_run window)
   // KREG = 0 generator scratch (sized as smem_rows in lp_api.cpp): the
   // displacement list MAP[i * T], or for n <= 256 the displaced bitmap
   // DIS[w * T] followed by the byte position table.
@@ -398,7 +466,7 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
   for (uint64_t t = w.t0 + tid; t < w.t1; t += T) {
     uint32_t s0 = 0;
     uint32_t sl[KS];  // KREG > 0: the sorted slots (padding 0xffffffff)
-    for (int i = 0; i <= nw; ++i) BMc[i * T] = 0u;
+    for (int i = 0; i < nw + 3; ++i) BMc[i * T] = 0u;
     if (KREG > 0) {
       if (pd.exact) gen_exact_regs<KS>(t, n, k, binom + pd.binom_off, pd.binom_stride, sl);
       else gen_mc_regs<KS>(pd.seed, t, k, dc, sl);
