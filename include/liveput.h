@@ -33,7 +33,9 @@ typedef enum {
   LP_ECUDA = 2,        /* CUDA runtime failure */
   LP_ENOMEM = 3,       /* device or host allocation failed */
   LP_EUNSUPPORTED = 4, /* outside the sizes this build supports */
-  LP_ENCCL = 5         /* NCCL failure */
+  LP_ENCCL = 5,        /* NCCL failure */
+  LP_EROLLBACK = 6     /* plan_migration: a stage lost every replica (RollbackRequired,
+                          migration.hpp:49-51) */
 } lp_status;
 
 /* ParallelConfig (perf_model.hpp:10-16). pipelines == 0 -> suspended. */
@@ -222,6 +224,99 @@ int32_t lp_enumerate_configs(const lp_profile* profile, int32_t n, lp_config* ou
 int32_t lp_reactive_plan(const lp_profile* profile, int32_t n_now, lp_config* out);
 uint64_t lp_scenario_count(int32_t n, int32_t k);
 uint64_t lp_mix_seed(uint64_t a, uint64_t b);
+
+/* ---- migration planning for a realised scenario:
+ *      plan_migration migration.cpp:106-217, migration_cost :219-236,
+ *      transition_outcome_min :49-89, resume_cost :100-104.  Host code: the
+ *      concrete moves of the one transition the DP chose, not a hot path. -- */
+typedef enum {
+  LP_MIG_NONE = 0, /* MigrationKind (migration.hpp:11) */
+  LP_MIG_INTRA_STAGE = 1,
+  LP_MIG_INTER_STAGE = 2,
+  LP_MIG_PIPELINE = 3
+} lp_migration_kind;
+
+/* Move (migration.hpp:29-34).  from_pipeline = from_stage = -1 for a spare. */
+typedef struct {
+  int32_t instance;
+  int32_t from_pipeline, from_stage;
+  int32_t to_pipeline, to_stage;
+  int32_t transfers_params; /* 0 / 1 */
+} lp_move;
+
+/* MigrationPlan (migration.hpp:36-43) without the move vector. */
+typedef struct {
+  int32_t kind; /* lp_migration_kind */
+  int32_t transfer_rounds;
+  lp_config source;
+  lp_config target;
+  double est_cost_s;
+  int32_t n_moves; /* moves in the plan (may exceed the caller's cap) */
+  int32_t pad;
+} lp_migration;
+
+/* Plans the transition from `source` (+ `spares` trailing spare instances)
+ * to `target` under the preemption vector v[0 .. source.D*source.P+spares)
+ * (v[k] = 1: instance k preempted).  Writes min(n_moves, cap) moves in the
+ * reference's order.  LP_EROLLBACK when a stage has no survivor and the
+ * target keeps a pipeline; LP_EINVAL on a size mismatch or too few bodies. */
+lp_status lp_plan_migration(const lp_profile* profile, const lp_costs* costs, lp_config source,
+                            int32_t spares, const uint8_t* v, int32_t v_len, lp_config target,
+                            lp_migration* out, lp_move* moves, int32_t cap);
+/* T_mig of a plan (migration_cost); fresh_instances > 0 adds process startup. */
+double lp_migration_cost(const lp_profile* profile, const lp_costs* costs, const lp_migration* plan,
+                         int32_t fresh_instances);
+/* Stats-level costing from the per-stage survivor minimum. */
+lp_status lp_transition_outcome(const lp_profile* profile, const lp_costs* costs,
+                                int32_t min_survivor, lp_config source, lp_config target,
+                                int32_t fresh_instances, double* cost_s, int32_t* kind,
+                                int32_t* rollback);
+double lp_resume_cost(const lp_profile* profile, const lp_costs* costs, lp_config target);
+
+/* ---- availability forecasts, the DP's n_seq producer:
+ *      predict predictor.cpp:239-274 (preprocess :29-77, ARIMA(2,1,2) two-
+ *      stage least squares :81-188, postprocess :190-237), eval_l1 :276-286,
+ *      and the sliding-window evaluation of `spotsim predict`
+ *      (tools/commands.cpp:267-299).  One device thread per (window, method);
+ *      FP64 without contraction, so forecasts are bit-identical. ---------- */
+typedef enum {
+  LP_PREDICT_ARIMA = 0, /* PredictMethod (predictor.hpp:25) */
+  LP_PREDICT_MOVING_AVG = 1,
+  LP_PREDICT_EXP_SMOOTH = 2,
+  LP_PREDICT_LAST_VALUE = 3
+} lp_predict_method;
+
+/* ForecastConfig (predictor.hpp:8-18). */
+typedef struct {
+  int32_t history_len;
+  int32_t lookahead;
+  int32_t capacity;
+  int32_t floor;
+  int32_t max_step;
+  int32_t reset_threshold;
+  int32_t moving_avg_window;
+  int32_t pad;
+  double exp_smooth_factor;
+  double steep_decay;
+} lp_forecast_config;
+
+/* The reference's defaults (history 12, lookahead 12, max_step 8, ...). */
+lp_forecast_config lp_forecast_defaults(int32_t capacity);
+/* predict(): forecast of the next cfg->lookahead counts from the last
+ * cfg->history_len entries of history[0 .. len).  out: lookahead ints.
+ * LP_EINVAL when len < history_len or lookahead < 1. */
+lp_status lp_predict(const int32_t* history, int32_t len, const lp_forecast_config* cfg,
+                     int32_t method, int32_t device, int32_t* out);
+/* Every window t = H .. len-I of counts (history counts[t-H, t), actual
+ * counts[t, t+I)) for each method: preds[(w*n_methods + m)*I + j] and, when
+ * l1 is not null, l1[w*n_methods + m] = eval_l1.  *n_windows receives the
+ * window count (0 when len < H + I). */
+lp_status lp_predict_windows(const int32_t* counts, int32_t len, const lp_forecast_config* cfg,
+                             const int32_t* methods, int32_t n_methods, int32_t device,
+                             int32_t* preds, double* l1, int32_t* n_windows);
+/* (sum |pred - actual|) / (sum actual); 0 for an exact all-zero match, +inf
+ * when actual sums to zero and pred does not. */
+double lp_eval_l1(const int32_t* pred, const int32_t* actual, int32_t len);
 
 /* Build information (sm arch, sizes supported). */
 int32_t lp_max_instances(void);

@@ -261,4 +261,102 @@ inline double expected_liveput(Planner& planner, const ParallelConfig& cfg, int 
   return v;
 }
 
+// ---- migration.hpp:11-101 — concrete moves for a realised scenario ------
+enum class MigrationKind { none, intra_stage, inter_stage, pipeline };
+
+struct Topology {  // preemption.hpp:13-20
+  int pipelines = 0;
+  int stages = 0;
+  int spares = 0;
+  int assigned() const { return pipelines * stages; }
+  int total() const { return assigned() + spares; }
+};
+
+using PreemptionVector = std::vector<uint8_t>;
+
+struct Move {
+  int instance = 0;
+  int from_pipeline = 0, from_stage = 0;
+  int to_pipeline = 0, to_stage = 0;
+  bool transfers_params = false;
+};
+
+struct MigrationPlan {
+  MigrationKind kind = MigrationKind::none;
+  std::vector<Move> moves;
+  ParallelConfig source;
+  ParallelConfig target;
+  int transfer_rounds = 0;
+  double est_cost_s = 0.0;
+};
+
+struct RollbackRequired : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct TransitionOutcome {
+  double cost_s = 0.0;
+  MigrationKind kind = MigrationKind::none;
+  bool rollback = false;
+};
+
+inline MigrationPlan plan_migration(const Topology& topo, const PreemptionVector& v,
+                                    const ParallelConfig& target, const WorkloadProfile& w,
+                                    const CostTable& costs) {
+  detail::ProfileC p(w);
+  const lp_costs c = detail::to_c(costs);
+  lp_migration out{};
+  std::vector<lp_move> mv(v.size() + 1);
+  const lp_status s = lp_plan_migration(&p.p, &c, {topo.pipelines, topo.stages}, topo.spares, v.data(),
+                                        static_cast<int32_t>(v.size()), {target.pipelines, target.stages},
+                                        &out, mv.data(), static_cast<int32_t>(mv.size()));
+  if (s == LP_EROLLBACK) throw RollbackRequired(lp_last_global_error());
+  detail::check(s, nullptr);
+  MigrationPlan plan;
+  plan.kind = static_cast<MigrationKind>(out.kind);
+  plan.source = {out.source.pipelines, out.source.stages};
+  plan.target = {out.target.pipelines, out.target.stages};
+  plan.transfer_rounds = out.transfer_rounds;
+  plan.est_cost_s = out.est_cost_s;
+  for (int i = 0; i < out.n_moves; ++i)
+    plan.moves.push_back({mv[i].instance, mv[i].from_pipeline, mv[i].from_stage, mv[i].to_pipeline,
+                          mv[i].to_stage, mv[i].transfers_params != 0});
+  return plan;
+}
+
+inline double migration_cost(const MigrationPlan& plan, const WorkloadProfile& w,
+                             const CostTable& costs, int fresh_instances) {
+  detail::ProfileC p(w);
+  const lp_costs c = detail::to_c(costs);
+  lp_migration m{};
+  m.kind = static_cast<int32_t>(plan.kind);
+  m.transfer_rounds = plan.transfer_rounds;
+  m.source = {plan.source.pipelines, plan.source.stages};
+  m.target = {plan.target.pipelines, plan.target.stages};
+  return lp_migration_cost(&p.p, &c, &m, fresh_instances);
+}
+
+inline TransitionOutcome transition_outcome_min(int min_survivor, const ParallelConfig& source,
+                                                const ParallelConfig& target, int fresh_instances,
+                                                const WorkloadProfile& w, const CostTable& costs) {
+  detail::ProfileC p(w);
+  const lp_costs c = detail::to_c(costs);
+  TransitionOutcome o;
+  int32_t kind = 0, rb = 0;
+  detail::check(lp_transition_outcome(&p.p, &c, min_survivor, {source.pipelines, source.stages},
+                                      {target.pipelines, target.stages}, fresh_instances, &o.cost_s,
+                                      &kind, &rb),
+                nullptr);
+  o.kind = static_cast<MigrationKind>(kind);
+  o.rollback = rb != 0;
+  return o;
+}
+
+inline double resume_cost(const ParallelConfig& target, const WorkloadProfile& w,
+                          const CostTable& costs) {
+  detail::ProfileC p(w);
+  const lp_costs c = detail::to_c(costs);
+  return lp_resume_cost(&p.p, &c, {target.pipelines, target.stages});
+}
+
 }  // namespace spotsim_b200

@@ -121,6 +121,10 @@ def ref_lib():
             "ref_expected_liveput": (C.c_int, [prof] + [C.c_int] * 6 + [C.c_uint64, _P(C.c_double)]),
             "ref_transition_outcome_min": (C.c_int, [C.c_int] * 6 + [prof, costs, _P(C.c_double)]),
             "ref_resume_cost": (C.c_double, [C.c_int, C.c_int, prof, costs]),
+            "ref_predict": (C.c_int, [_P(C.c_int), C.c_int, _P(C.c_int), _P(C.c_double), C.c_int, _P(C.c_int)]),
+            "ref_eval_l1": (C.c_double, [_P(C.c_int), _P(C.c_int), C.c_int]),
+            "ref_plan_migration": (C.c_int, [C.c_int] * 3 + [_P(C.c_uint8), C.c_int, C.c_int, C.c_int, prof, costs,
+                                             _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_double)]),
             "ref_gen_synthetic": (C.c_int, [C.c_uint64] + [C.c_int] * 6 + [_P(C.c_int), C.c_int]),
             "ref_bench_histograms": (C.c_double, [prof, costs, opts, _P(C.c_int), _P(C.c_int), C.c_int, C.c_int,
                                                   _P(C.c_ulonglong)]),
@@ -317,3 +321,65 @@ def mix_seed(a, b):
 def planner_seed(mc_seed, n, k):
     """optimizer.cpp:88-89: mix_seed(mix_seed(mc_seed, n), k)."""
     return mix_seed(mix_seed(mc_seed, n), k)
+
+
+def ref_plan_migration(w: WorkloadProfile, costs: CostTable, source: ParallelConfig, spares: int, v,
+                       target: ParallelConfig):
+    """The reference's plan_migration through oracle/_ref (test infrastructure).
+    Returns ("ok", kind, rounds, moves, est_cost, cost_fresh) or ("rollback",) /
+    ("invalid",)."""
+    l = ref_lib()
+    p, keep = w.to_c()
+    c = costs.to_c()
+    n = len(v)
+    vb = (C.c_uint8 * max(n, 1))(*[1 if x else 0 for x in v])
+    info = (C.c_int * 3)()
+    cap = max(n, 1)
+    mv = (C.c_int * (6 * cap))()
+    cost = (C.c_double * 2)()
+    rc = l.ref_plan_migration(source.pipelines, source.stages, spares, vb, n, target.pipelines, target.stages,
+                              C.byref(p), C.byref(c), info, mv, cap, cost)
+    if rc == 1:
+        return ("rollback",)
+    if rc == 2:
+        return ("invalid",)
+    moves = [tuple(mv[6 * i: 6 * i + 6]) for i in range(min(info[2], cap))]
+    return ("ok", info[0], info[1], moves, cost[0], cost[1])
+
+
+def ref_transition_outcome(w: WorkloadProfile, costs: CostTable, m, sd, sp, td, tp, fresh):
+    """The reference's transition_outcome_min: (cost_s, kind name, rollback)."""
+    l = ref_lib()
+    p, keep = w.to_c()
+    c = costs.to_c()
+    out = (C.c_double * 2)()
+    kind = l.ref_transition_outcome_min(m, sd, sp, td, tp, fresh, C.byref(p), C.byref(c), out)
+    names = {0: "none", 1: "intra_stage", 2: "inter_stage", 3: "pipeline"}
+    return out[0], names[kind], bool(out[1])
+
+
+def ref_predict(history, cfg, method: int):
+    """The reference's predict() through oracle/_ref; None on invalid_argument."""
+    l = ref_lib()
+    h = (C.c_int * max(len(history), 1))(*history)
+    ci = (C.c_int * 7)(cfg.history_len, cfg.lookahead, cfg.capacity, cfg.floor, cfg.max_step,
+                       cfg.reset_threshold, cfg.moving_avg_window)
+    cd = (C.c_double * 2)(cfg.exp_smooth_factor, cfg.steep_decay)
+    out = (C.c_int * max(cfg.lookahead, 1))()
+    if l.ref_predict(h, len(history), ci, cd, method, out) != 0:
+        return None
+    return list(out[: cfg.lookahead])
+
+
+def ref_eval_l1(pred, actual):
+    l = ref_lib()
+    a = (C.c_int * max(len(pred), 1))(*pred)
+    b = (C.c_int * max(len(actual), 1))(*actual)
+    return l.ref_eval_l1(a, b, len(pred))
+
+
+def ref_gen_synthetic(seed, cap, length, loss_events, gain_events, min_step, max_step):
+    l = ref_lib()
+    out = (C.c_int * (length + 8))()
+    n = l.ref_gen_synthetic(seed, cap, length, loss_events, gain_events, min_step, max_step, out, length + 8)
+    return list(out[:n])

@@ -270,6 +270,76 @@ double ref_resume_cost(int td, int tp, const lp_profile* p, const lp_costs* c) {
   return resume_cost({td, tp}, to_profile(p), to_costs(c));
 }
 
+// plan_migration (migration.cpp:106-217) + migration_cost (:219-236).
+// moves_out: 6 ints per move (instance, from_pipeline, from_stage,
+// to_pipeline, to_stage, transfers_params).  info_out: {kind, transfer_rounds,
+// n_moves}.  cost_out: {est_cost_s, migration_cost(fresh = 1)}.  Returns 0,
+// 1 for RollbackRequired, 2 for std::invalid_argument.
+int ref_plan_migration(int sd, int sp, int spares, const uint8_t* v, int v_len, int td, int tp,
+                       const lp_profile* p, const lp_costs* c, int* info_out, int* moves_out,
+                       int cap, double* cost_out) {
+  try {
+    const Topology topo{sd, sp, spares};
+    PreemptionVector vec(v, v + v_len);
+    const WorkloadProfile w = to_profile(p);
+    const CostTable costs = to_costs(c);
+    MigrationPlan plan = plan_migration(topo, vec, {td, tp}, w, costs);
+    info_out[0] = (int)plan.kind;
+    info_out[1] = plan.transfer_rounds;
+    info_out[2] = (int)plan.moves.size();
+    for (int i = 0; i < (int)plan.moves.size() && i < cap; ++i) {
+      const Move& m = plan.moves[i];
+      int* o = moves_out + 6 * i;
+      o[0] = m.instance;
+      o[1] = m.from_pipeline;
+      o[2] = m.from_stage;
+      o[3] = m.to_pipeline;
+      o[4] = m.to_stage;
+      o[5] = m.transfers_params ? 1 : 0;
+    }
+    cost_out[0] = plan.est_cost_s;
+    cost_out[1] = migration_cost(plan, w, costs, 1);
+    return 0;
+  } catch (const RollbackRequired& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// predict (predictor.cpp:239-274): cfg9 = {history_len, lookahead, capacity,
+// floor, max_step, reset_threshold, moving_avg_window} ints + {exp_smooth,
+// steep_decay} doubles.  Returns 0, or 2 on std::invalid_argument.
+int ref_predict(const int* history, int len, const int* cfg_i, const double* cfg_d, int method,
+                int* out) {
+  try {
+    ForecastConfig fc;
+    fc.history_len = cfg_i[0];
+    fc.lookahead = cfg_i[1];
+    fc.capacity = cfg_i[2];
+    fc.floor = cfg_i[3];
+    fc.max_step = cfg_i[4];
+    fc.reset_threshold = cfg_i[5];
+    fc.moving_avg_window = cfg_i[6];
+    fc.exp_smooth_factor = cfg_d[0];
+    fc.steep_decay = cfg_d[1];
+    const Forecast f = predict(std::vector<int>(history, history + len), fc, (PredictMethod)method);
+    for (size_t i = 0; i < f.values.size(); ++i) out[i] = f.values[i];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+double ref_eval_l1(const int* pred, const int* actual, int len) {
+  Forecast f;
+  f.values.assign(pred, pred + len);
+  return eval_l1(f, std::vector<int>(actual, actual + len));
+}
+
 // gen_synthetic (trace.cpp:80-180): writes up to cap counts, returns length.
 int ref_gen_synthetic(uint64_t seed, int cap, int length, int loss_events, int gain_events,
                       int min_step, int max_step, int* out, int out_cap) {

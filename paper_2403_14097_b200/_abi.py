@@ -13,7 +13,9 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "lib" / "libliveput.so"
 
-LP_OK, LP_EINVAL, LP_ECUDA, LP_ENOMEM, LP_EUNSUPPORTED, LP_ENCCL = range(6)
+LP_OK, LP_EINVAL, LP_ECUDA, LP_ENOMEM, LP_EUNSUPPORTED, LP_ENCCL, LP_EROLLBACK = range(7)
+LP_MIG_NONE, LP_MIG_INTRA_STAGE, LP_MIG_INTER_STAGE, LP_MIG_PIPELINE = range(4)
+LP_PREDICT_ARIMA, LP_PREDICT_MOVING_AVG, LP_PREDICT_EXP_SMOOTH, LP_PREDICT_LAST_VALUE = range(4)
 LP_NCCL_ID_BYTES = 128
 
 
@@ -96,8 +98,30 @@ class lp_stats(C.Structure):
     ]
 
 
+class lp_move(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("from_pipeline", C.c_int32), ("from_stage", C.c_int32),
+                ("to_pipeline", C.c_int32), ("to_stage", C.c_int32), ("transfers_params", C.c_int32)]
+
+
+class lp_migration(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("transfer_rounds", C.c_int32), ("source", lp_config),
+                ("target", lp_config), ("est_cost_s", C.c_double), ("n_moves", C.c_int32),
+                ("pad", C.c_int32)]
+
+
+class lp_forecast_config(C.Structure):
+    _fields_ = [("history_len", C.c_int32), ("lookahead", C.c_int32), ("capacity", C.c_int32),
+                ("floor", C.c_int32), ("max_step", C.c_int32), ("reset_threshold", C.c_int32),
+                ("moving_avg_window", C.c_int32), ("pad", C.c_int32), ("exp_smooth_factor", C.c_double),
+                ("steep_decay", C.c_double)]
+
+
 class LiveputError(RuntimeError):
     pass
+
+
+class RollbackRequired(LiveputError):
+    """migration.hpp:49-51: a stage lost every replica; restore from checkpoint."""
 
 
 _lib = None
@@ -136,6 +160,18 @@ _SIGS = {
     "lp_reactive_plan": (C.c_int32, [_P(lp_profile), C.c_int32, _P(lp_config)]),
     "lp_scenario_count": (C.c_uint64, [C.c_int32, C.c_int32]),
     "lp_mix_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "lp_plan_migration": (C.c_int, [_P(lp_profile), _P(lp_costs), lp_config, C.c_int32, _P(C.c_uint8),
+                                    C.c_int32, lp_config, _P(lp_migration), _P(lp_move), C.c_int32]),
+    "lp_migration_cost": (C.c_double, [_P(lp_profile), _P(lp_costs), _P(lp_migration), C.c_int32]),
+    "lp_transition_outcome": (C.c_int, [_P(lp_profile), _P(lp_costs), C.c_int32, lp_config, lp_config,
+                                        C.c_int32, _P(C.c_double), _P(C.c_int32), _P(C.c_int32)]),
+    "lp_resume_cost": (C.c_double, [_P(lp_profile), _P(lp_costs), lp_config]),
+    "lp_forecast_defaults": (lp_forecast_config, [C.c_int32]),
+    "lp_predict": (C.c_int, [_P(C.c_int32), C.c_int32, _P(lp_forecast_config), C.c_int32, C.c_int32,
+                             _P(C.c_int32)]),
+    "lp_predict_windows": (C.c_int, [_P(C.c_int32), C.c_int32, _P(lp_forecast_config), _P(C.c_int32), C.c_int32,
+                                     C.c_int32, _P(C.c_int32), _P(C.c_double), _P(C.c_int32)]),
+    "lp_eval_l1": (C.c_double, [_P(C.c_int32), _P(C.c_int32), C.c_int32]),
     "lp_max_instances": (C.c_int32, []),
     "lp_build_info": (C.c_char_p, []),
 }
@@ -185,4 +221,6 @@ def check(status, handle=None):
     msg = msg.decode() if msg else ""
     if status == LP_EINVAL:
         raise ValueError(msg)
+    if status == LP_EROLLBACK:
+        raise RollbackRequired(msg)
     raise LiveputError(f"liveput status {status}: {msg}")

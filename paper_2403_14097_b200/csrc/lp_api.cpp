@@ -26,6 +26,12 @@ namespace lp {
 namespace {
 
 thread_local std::string g_global_err;
+}  // namespace
+
+// lp_migration.cpp reports through the same per-thread message
+std::string& global_error() { return g_global_err; }
+
+namespace {
 
 constexpr uint64_t kEnumerationCap = 1000000ULL;  // preemption.hpp:26
 constexpr size_t kSmemBudgetR = 72 * 1024;

@@ -229,3 +229,149 @@ def scenario_count(n: int, k: int) -> int:
 
 def mix_seed(a: int, b: int) -> int:
     return _abi.lib().lp_mix_seed(a, b)
+
+
+# ---- migration planning for a realised scenario ----------
+RollbackRequired = _abi.RollbackRequired
+MIGRATION_KINDS = {_abi.LP_MIG_NONE: "none", _abi.LP_MIG_INTRA_STAGE: "intra_stage",
+                   _abi.LP_MIG_INTER_STAGE: "inter_stage", _abi.LP_MIG_PIPELINE: "pipeline"}
+
+
+@dataclass
+class Move:
+    """Move (migration.hpp:29-34); from_* are -1 for a spare instance."""
+    instance: int
+    from_pipeline: int
+    from_stage: int
+    to_pipeline: int
+    to_stage: int
+    transfers_params: bool
+
+
+@dataclass
+class MigrationPlan:
+    """MigrationPlan (migration.hpp:36-43)."""
+    kind: str
+    moves: List[Move]
+    source: ParallelConfig
+    target: ParallelConfig
+    transfer_rounds: int
+    est_cost_s: float
+    _c: object = None
+
+    def cost(self, w: WorkloadProfile, costs: CostTable, fresh_instances: int = 0) -> float:
+        """migration_cost (migration.cpp:219-236)."""
+        p, keep = w.to_c()
+        c = costs.to_c()
+        return _abi.lib().lp_migration_cost(C.byref(p), C.byref(c), C.byref(self._c), fresh_instances)
+
+
+def plan_migration(source: ParallelConfig, spares: int, v: Sequence[int], target: ParallelConfig,
+                   w: WorkloadProfile, costs: CostTable) -> MigrationPlan:
+    """plan_migration (migration.cpp:106-217) for topology (source, spares) under
+    preemption vector v (1 = preempted).  Raises RollbackRequired when a stage has
+    no survivor, ValueError on a size mismatch or too few instances."""
+    lib = _abi.lib()
+    p, keep = w.to_c()
+    c = costs.to_c()
+    n = len(v)
+    vb = (C.c_uint8 * max(n, 1))(*[1 if x else 0 for x in v])
+    out = _abi.lp_migration()
+    cap = max(n, 1)
+    moves = (_abi.lp_move * cap)()
+    _abi.check(lib.lp_plan_migration(C.byref(p), C.byref(c), source.to_c(), spares, vb, n, target.to_c(),
+                                     C.byref(out), moves, cap))
+    mv = [Move(m.instance, m.from_pipeline, m.from_stage, m.to_pipeline, m.to_stage, bool(m.transfers_params))
+          for m in moves[: min(out.n_moves, cap)]]
+    return MigrationPlan(MIGRATION_KINDS[out.kind], mv, ParallelConfig(out.source.pipelines, out.source.stages),
+                         ParallelConfig(out.target.pipelines, out.target.stages), out.transfer_rounds,
+                         out.est_cost_s, out)
+
+
+def transition_outcome(min_survivor: int, source: ParallelConfig, target: ParallelConfig,
+                       fresh_instances: int, w: WorkloadProfile, costs: CostTable) -> Tuple[float, str, bool]:
+    """transition_outcome_min (migration.cpp:49-89): (cost_s, kind, rollback)."""
+    p, keep = w.to_c()
+    c = costs.to_c()
+    cost, kind, rb = C.c_double(), C.c_int32(), C.c_int32()
+    _abi.check(_abi.lib().lp_transition_outcome(C.byref(p), C.byref(c), min_survivor, source.to_c(),
+                                                target.to_c(), fresh_instances, C.byref(cost), C.byref(kind),
+                                                C.byref(rb)))
+    return cost.value, MIGRATION_KINDS[kind.value], bool(rb.value)
+
+
+def resume_cost(target: ParallelConfig, w: WorkloadProfile, costs: CostTable) -> float:
+    """resume_cost (migration.cpp:100-104)."""
+    p, keep = w.to_c()
+    c = costs.to_c()
+    return _abi.lib().lp_resume_cost(C.byref(p), C.byref(c), target.to_c())
+
+
+# ---- availability forecasts: the DP's n_seq producer (SURVEY.md §8f #4) ------
+PREDICT_METHODS = {"arima": _abi.LP_PREDICT_ARIMA, "moving_avg": _abi.LP_PREDICT_MOVING_AVG,
+                   "exp_smooth": _abi.LP_PREDICT_EXP_SMOOTH, "last_value": _abi.LP_PREDICT_LAST_VALUE}
+
+
+@dataclass
+class ForecastConfig:
+    """ForecastConfig (predictor.hpp:8-18)."""
+    history_len: int = 12
+    lookahead: int = 12
+    capacity: int = 0
+    floor: int = 0
+    max_step: int = 8
+    reset_threshold: int = 10
+    moving_avg_window: int = 4
+    exp_smooth_factor: float = 0.5
+    steep_decay: float = 0.7
+
+    def to_c(self) -> _abi.lp_forecast_config:
+        return _abi.lp_forecast_config(self.history_len, self.lookahead, self.capacity, self.floor,
+                                       self.max_step, self.reset_threshold, self.moving_avg_window, 0,
+                                       self.exp_smooth_factor, self.steep_decay)
+
+
+def _method(m) -> int:
+    if isinstance(m, str):
+        if m not in PREDICT_METHODS:
+            raise ValueError(f"unknown predict method: {m}")
+        return PREDICT_METHODS[m]
+    return int(m)
+
+
+def predict(history: Sequence[int], cfg: ForecastConfig, method="arima", device: int = 0) -> List[int]:
+    """predict (predictor.cpp:239-274), evaluated on the GPU."""
+    h = (C.c_int32 * max(len(history), 1))(*history)
+    out = (C.c_int32 * max(cfg.lookahead, 1))()
+    c = cfg.to_c()
+    _abi.check(_abi.lib().lp_predict(h, len(history), C.byref(c), _method(method), device, out))
+    return list(out[: cfg.lookahead])
+
+
+def predict_windows(counts: Sequence[int], cfg: ForecastConfig, methods=("arima",), device: int = 0):
+    """Every sliding window of `spotsim predict` (commands.cpp:267-299) at once:
+    returns (preds[window][method] -> list, l1[window][method])."""
+    ms = [_method(m) for m in methods]
+    n = len(counts)
+    nw = max(0, n - cfg.history_len - cfg.lookahead + 1)
+    cnt = (C.c_int32 * max(n, 1))(*counts)
+    mth = (C.c_int32 * len(ms))(*ms)
+    preds = (C.c_int32 * max(nw * len(ms) * cfg.lookahead, 1))()
+    l1 = (C.c_double * max(nw * len(ms), 1))()
+    got = C.c_int32()
+    c = cfg.to_c()
+    _abi.check(_abi.lib().lp_predict_windows(cnt, n, C.byref(c), mth, len(ms), device, preds, l1, C.byref(got)))
+    I, M = cfg.lookahead, len(ms)
+    P = [[list(preds[(w * M + m) * I:(w * M + m + 1) * I]) for m in range(M)] for w in range(got.value)]
+    L = [[l1[w * M + m] for m in range(M)] for w in range(got.value)]
+    return P, L
+
+
+def eval_l1(pred: Sequence[int], actual: Sequence[int]) -> float:
+    """eval_l1 (predictor.cpp:276-286)."""
+    if len(pred) != len(actual):
+        raise ValueError("eval_l1: length mismatch")
+    n = len(pred)
+    a = (C.c_int32 * max(n, 1))(*pred)
+    b = (C.c_int32 * max(n, 1))(*actual)
+    return _abi.lib().lp_eval_l1(a, b, n)

@@ -225,6 +225,38 @@ int main() {
     }
     EXPECT(thrown);
   }
+  // ---- migration planning (test_migration.cpp:8-75 behaviours)
+  {
+    const WorkloadProfile w = lm_1p5b();
+    const CostTable costs;
+    PreemptionVector none(12, 0);
+    MigrationPlan keep = plan_migration(Topology{3, 4, 0}, none, {3, 4}, w, costs);
+    EXPECT(keep.kind == MigrationKind::none && keep.moves.empty() && keep.est_cost_s == 0.0);
+    PreemptionVector two(12, 0);
+    two[0] = 1;
+    two[5] = 1;
+    MigrationPlan intra = plan_migration(Topology{3, 4, 0}, two, {2, 4}, w, costs);
+    EXPECT(intra.kind == MigrationKind::intra_stage && intra.moves.size() == 1 &&
+           !intra.moves[0].transfers_params);
+    PreemptionVector lost(6, 0);
+    lost[1] = 1;
+    lost[4] = 1;
+    bool rolled = false;
+    try {
+      plan_migration(Topology{2, 3, 0}, lost, {1, 3}, w, costs);
+    } catch (const RollbackRequired&) {
+      rolled = true;
+    }
+    EXPECT(rolled);
+    PreemptionVector hole(17, 0);
+    hole[3] = 1;
+    MigrationPlan inter = plan_migration(Topology{2, 8, 1}, hole, {2, 8}, w, costs);
+    EXPECT(inter.kind == MigrationKind::inter_stage && inter.transfer_rounds == 1);
+    EXPECT(migration_cost(inter, w, costs, 0) == inter.est_cost_s);
+    const TransitionOutcome t = transition_outcome_min(0, {4, 8}, {3, 8}, 0, w, costs);
+    EXPECT(t.rollback && t.kind == MigrationKind::pipeline);
+    EXPECT(resume_cost({3, 8}, w, costs) > t.cost_s);
+  }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
