@@ -1,11 +1,15 @@
 """BASELINE config 3: GPT-3 6.7B (D,P) table, N=128, 1e6 samples/point, the
 strategy-sequence replay of a synthetic 24 h trace (1440 one-minute intervals).
 
-The planning loop is the Ideal(12) policy of the reference simulator
-(simulator.cpp:301-318, Policy::Ideal): at interval i the planner sees the true
-next 12 availability counts and `current` is the configuration committed for
-interval i, which under Ideal is the previous plan's first step (it always fits,
-so adjust_config leaves it unchanged).  One Planner persists across the replay,
+Two planning loops of the reference simulator (simulator.cpp:185-199, 296-318):
+  --policy ideal      Ideal(12): at interval i the planner sees the true next 12
+                      availability counts; `current` is the previous plan's first
+                      step (it always fits, so adjust_config leaves it unchanged).
+  --policy proactive  Proactive(12, arima, 12): n_seq = [n_i] + predict(history)
+                      and `current` = adjust_config(previous plan's first step,
+                      n_i).  On the GPU every interval's forecast comes from ONE
+                      lp_predict_windows launch over the trace (the history never
+                      depends on the decisions), included in the timed total.  One Planner persists across the replay,
 as in the CLI (commands.cpp:215-216), so ensembles seen before come from the
 histogram cache — the reference's hist_cache_ — on the GPU too.
 
@@ -57,12 +61,57 @@ def loop(plan_fn, reactive_fn, counts, intervals):
     return seq, times
 
 
+def adjust_config(planned, n, depth_ok):
+    """simulator.cpp:31-43."""
+    if planned is not None:
+        if n >= planned.pipelines * planned.stages:
+            return planned
+        d = n // planned.stages
+        if d >= 1:
+            return type(planned)(d, planned.stages)
+    for p in range(n, 0, -1):
+        if depth_ok(p):
+            return type(planned)(1, p) if planned is not None else _cfg(1, p)
+    return None
+
+
+def _cfg(d, p):
+    from paper_2403_14097_b200.model import ParallelConfig
+    return ParallelConfig(d, p)
+
+
+def padded_history(counts, i, H):
+    """History at interval i (counts[0..i]) left-padded with its first value to H
+    entries, as simulator.cpp:311-313 does before predict()."""
+    h = counts[: i + 1]
+    return [h[0]] * max(0, H - len(h)) + h
+
+
+def loop_proactive(plan_fn, reactive_fn, forecast_fn, depth_ok, counts, intervals):
+    seq, times = [], []
+    last = min(intervals, len(counts))
+    cfg, planned = reactive_fn(counts[0]), None
+    for i in range(last):
+        n = counts[i]
+        if i > 0:
+            cfg = adjust_config(planned, n, depth_ok)
+        ns = [n] + forecast_fn(i)
+        t = time.perf_counter()
+        plan = plan_fn(cfg, ns)
+        times.append(time.perf_counter() - t)
+        planned = plan[0].config
+        seq.append([[planned.pipelines, planned.stages] if planned else None, plan[0].expected_committed.hex(),
+                    plan[0].expected_mig_cost_s.hex(), ns[1:]])
+    return seq, times
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("mode", choices=["trace", "gpu", "ref", "compare"])
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--intervals", type=int, default=1440)
     ap.add_argument("--no-cache", action="store_true")
+    ap.add_argument("--policy", choices=["ideal", "proactive"], default="ideal")
     ap.add_argument("--out", default=None)
     ap.add_argument("files", nargs="*")
     a = ap.parse_args()
@@ -79,21 +128,43 @@ def main():
     from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_6p7b
     w = lm_6p7b()
     opt = PlannerOptions(mc_trials=a.trials)
+    H = I = LOOKAHEAD
     if a.mode == "gpu":
-        from paper_2403_14097_b200.planner import Planner, reactive_plan
+        from paper_2403_14097_b200 import _abi
+        from paper_2403_14097_b200.planner import ForecastConfig, Planner, predict_windows, reactive_plan
         p = Planner(w, CostTable(), opt)
         if not a.no_cache:
             p.set_hist_cache(True)
         t0 = time.perf_counter()
-        seq, times = loop(p.dp_optimize, lambda n: reactive_plan(n, w), counts, a.intervals)
+        if a.policy == "ideal":
+            seq, times = loop(p.dp_optimize, lambda n: reactive_plan(n, w), counts, a.intervals)
+        else:
+            cap = json.loads(TRACE.read_text()).get("capacity", 128)
+            # window w of [c0]*(H-1) + counts + I pad values has history padded_history(counts, w, H)
+            series = [counts[0]] * (H - 1) + counts + [0] * I
+            preds, _ = predict_windows(series, ForecastConfig(history_len=H, lookahead=I, capacity=cap), ["arima"])
+            pw, keep = w.to_c()
+            depth_ok = lambda s: bool(_abi.lib().lp_depth_feasible(pw, s))
+            seq, times = loop_proactive(p.dp_optimize, lambda n: reactive_plan(n, w), lambda i: preds[i][0],
+                                        depth_ok, counts, a.intervals)
         total = time.perf_counter() - t0
     else:
-        from oracle.oracle import RefPlanner, oracle_reactive
-        p = RefPlanner(w, CostTable(), opt)
+        from oracle import oracle as O
+        from paper_2403_14097_b200.planner import ForecastConfig
+        p = O.RefPlanner(w, CostTable(), opt)
         t0 = time.perf_counter()
-        seq, times = loop(p.dp_optimize, lambda n: oracle_reactive(w, n), counts, a.intervals)
+        if a.policy == "ideal":
+            seq, times = loop(p.dp_optimize, lambda n: O.oracle_reactive(w, n), counts, a.intervals)
+        else:
+            cap = json.loads(TRACE.read_text()).get("capacity", 128)
+            fc = ForecastConfig(history_len=H, lookahead=I, capacity=cap)
+            pw, keep = w.to_c()
+            depth_ok = lambda s: bool(O.ref_lib().ref_depth_feasible(pw, s))
+            seq, times = loop_proactive(p.dp_optimize, lambda n: O.oracle_reactive(w, n),
+                                        lambda i: O.ref_predict(padded_history(counts, i, H), fc, 0),
+                                        depth_ok, counts, a.intervals)
         total = time.perf_counter() - t0
-    res = {"mode": a.mode, "trials": a.trials, "intervals": len(seq), "total_s": total,
+    res = {"mode": a.mode, "policy": a.policy, "trials": a.trials, "intervals": len(seq), "total_s": total,
            "mean_ms": 1e3 * total / max(1, len(seq)), "max_ms": 1e3 * max(times),
            "first_ms": 1e3 * times[0], "cache": not a.no_cache, "sequence": seq}
     print(json.dumps({k: v for k, v in res.items() if k != "sequence"}), flush=True)
