@@ -388,6 +388,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           T -= 32;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
+        auto& gv1 = groups[{4, kreg * 16 + wmax, T, sm ? 1 : 0}];
+        gv1.reserve(gv1.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -399,7 +401,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.smem_evt = sm ? 1 : 0;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + chunk);
-          groups[{4, kreg * 16 + wmax, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
+          gv1.push_back({w, {smem, 0}});
         }
         e = e2;
       }
@@ -430,6 +432,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T) > kSmemBudgetInc) T >>= 1;
         const size_t smem = smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
+        auto& gv2 = groups[{3, km, T, sm ? 1 : 0}];
+        gv2.reserve(gv2.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -443,7 +447,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.dtab_len = dlen;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + chunk);
-          groups[{3, km, T, sm ? 1 : 0}].push_back({w, {smem, 0}});
+          gv2.push_back({w, {smem, 0}});
         }
         e = e2;
       }
@@ -477,6 +481,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
+        auto& gv3 = groups[{2, kreg, T, sm ? 1 : 0}];
+        gv3.reserve(gv3.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -488,7 +494,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.smem_evt = sm ? 1 : 0;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + chunk);
-          groups[{2, kreg, T, sm ? 1 : 0}].push_back({w, {smem, uw}});
+          gv3.push_back({w, {smem, uw}});
         }
         e = e2;
       }
@@ -548,6 +554,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const bool sm = smem_ctr(e2 - e, pd.k, pd.n, ev, true, T, pmax) <= kSmemBudgetC;
         const size_t smem = smem_ctr(e2 - e, pd.k, pd.n, ev, sm, T, pmax);
         const uint64_t chunk = (uint64_t)T * 8;
+        auto& gv4 = groups[{1, 0, T, sm ? 1 : 0}];
+        gv4.reserve(gv4.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
           w.pair = pi;
@@ -558,7 +566,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.smem_evt = sm ? 1 : 0;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + chunk);
-          groups[{1, 0, T, sm ? 1 : 0}].push_back({w, {smem, pmax}});
+          gv4.push_back({w, {smem, pmax}});
         }
         e = e2;
       }
@@ -1090,6 +1098,11 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->horizon = H;
   h->levels.assign(H, LevelDesc{});
   h->cfg.clear();
+  {
+    size_t total = 1;
+    for (int j = 1; j <= H; ++j) total += h->model.configs(n_seq[j]).size() + 1;
+    h->cfg.reserve(total);
+  }
   std::vector<int> lbase(H + 1), lcount(H + 1);
   // level 0: current
   lbase[0] = 0;
@@ -1097,9 +1110,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->cfg.push_back({cur_on ? current.pipelines : 0, cur_on ? current.stages : 0, -1, 0});
   for (int j = 1; j <= H; ++j) {
     lbase[j] = (int)h->cfg.size();
-    for (const Cfg& c : h->model.configs(n_seq[j])) {
-      h->cfg.push_back({c.d, c.p, -1, 0});
-    }
+    for (const Cfg& c : h->model.configs(n_seq[j])) h->cfg.push_back({c.d, c.p, -1, 0});
     h->cfg.push_back({0, 0, -1, 0});  // suspension is always reachable
     lcount[j] = (int)h->cfg.size() - lbase[j];
   }

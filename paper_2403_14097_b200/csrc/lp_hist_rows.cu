@@ -60,6 +60,22 @@ __device__ __forceinline__ void emit_rises(M rises, uint32_t* eb, int eo, int Dm
   }
 }
 
+// The same rises accumulated in row order by shifting left (row x at bit
+// Dmax-1-x): emitted from the highest set bit down.
+template <bool SMEM_EVT, typename M>
+__device__ __forceinline__ void emit_rises_rev(M rises, uint32_t* eb, int eo, int Dm) {
+  constexpr int top = 8 * static_cast<int>(sizeof(M)) - 1;
+  auto msb = [](M r) { return top - (sizeof(M) == 8 ? __clzll(static_cast<long long>(r)) : __clz(static_cast<int>(r))); };
+  if (!rises) return;
+  rises ^= static_cast<M>(1) << msb(rises);  // the first rise is t = 1 (h0's event)
+  while (rises) {
+    const int b = msb(rises);
+    rises ^= static_cast<M>(1) << b;
+    evt_add<SMEM_EVT>(eb, eo + (Dm - 1 - b));
+    eo += Dm;
+  }
+}
+
 // Walk the rows of one depth.  BMc: this thread's bitmap column (stride T),
 // with at least one zero word past the last slot word.  Planes hold the
 // distance to the running maximum, dist = mx - count, in B bits per stage:
@@ -143,7 +159,7 @@ __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t 
     for (int l = 0; l < B; ++l) z |= Dp[l];
     const uint32_t hit = R & ~z;
     const uint32_t keep = hit ? 0u : 0xffffffffu;  // all-ones: decrement by R
-    rises |= static_cast<M>(hit != 0u) << x;
+    rises = rises + rises + static_cast<M>(keep + 1u);  // shift in (hit != 0)
     uint32_t c = R ^ (~keep & tmask);
 #pragma unroll
     for (int l = 0; l < B; ++l) {
@@ -152,14 +168,14 @@ __device__ __forceinline__ void walk_rows1(const uint32_t* BMc, int T, uint32_t 
       c = t;
     }
     sh += P;
-    if (sh >= 32u && x + 1 < Dm) {  // uniform across the warp; stays in the column
+    if (sh >= 32u) {  // uniform across the warp; the column has zero words past the slots
       sh -= 32u;
       w0 = w1;
       w1 = *next;
       next += T;
     }
   }
-  emit_rises<SMEM_EVT>(rises, eb, eoff, Dm);
+  emit_rises_rev<SMEM_EVT>(rises, eb, eoff, Dm);
 }
 
 // Depths with Dmax = DM <= 4 rows: the rows are unrolled at compile time and
