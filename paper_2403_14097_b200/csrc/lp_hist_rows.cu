@@ -92,6 +92,11 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
     for (int w = 0; w < W; ++w) Dp[l][w] = 0u;
   const uint32_t tail = P - 32u * (W - 1);  // bits in the last word (1..32)
   const uint32_t tmask = tail >= 32u ? 0xffffffffu : ((1u << tail) - 1u);
+  // rows where the maximum rose, shifted in (row x at bit Dm-1-x) when
+  // Dm <= 64 (always for W > 1: P > 32, Dm <= 512 / 33); emitted in the
+  // loop otherwise (one-word rows of P < n/64)
+  const bool masked = Dm <= 64;
+  unsigned long long rises = 0ull;
   int mx = 0;
   uint32_t pos = 0;
   for (int x = 0; x < Dm; ++x, pos += P) {
@@ -115,25 +120,27 @@ __device__ __forceinline__ void walk_rows(const uint32_t* BMc, int T, uint32_t P
     }
     // dist' = dist + inc - R with inc = (hit != 0): where R = 1 and inc = 1
     // nothing changes, so the update is one chain of +1 (inc) or -1 (!inc)
-    // over the mask c = inc ? ~R : R — branch-free, no divergence on events.
-    const bool inc = hit != 0;
-    if (inc) {
+    // over the mask c = inc ? ~R : R — branch-free.
+    const uint32_t keep = hit ? 0u : 0xffffffffu;
+    if (W > 1 || masked) {
+      rises = rises + rises + static_cast<unsigned long long>(keep + 1u);
+    } else if (hit) {
       ++mx;
       if (mx >= 2) evt_add<SMEM_EVT>(eb, eoff + (mx - 2) * Dm + x);
     }
-    const uint32_t flip = inc ? 0u : 0xffffffffu;  // borrow uses ~dist
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      uint32_t c = inc ? ~R[w] : R[w];
+      uint32_t c = R[w] ^ ~keep;
       if (w == W - 1) c &= tmask;
 #pragma unroll
       for (int l = 0; l < B; ++l) {
-        const uint32_t t = (Dp[l][w] ^ flip) & c;
+        const uint32_t t = (Dp[l][w] ^ keep) & c;
         Dp[l][w] ^= c;
         c = t;
       }
     }
   }
+  if (W > 1 || masked) emit_rises_rev<SMEM_EVT>(rises, eb, eoff, Dm);
 }
 
 // One-word rows (P <= 32) and at most 64 of them: the bitmap streams
