@@ -527,7 +527,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t& epoch) {
     const uint32_t target = epoch * gridDim.x;
     __threadfence();
     atomicAdd(ctr, 1u);
-    while (ld_relaxed_u32(ctr) < target) __nanosleep(20);
+    while (ld_relaxed_u32(ctr) < target) __nanosleep(100);
     __threadfence();  // acquire: orders the block's later reads after the arrivals
   }
   __syncthreads();
