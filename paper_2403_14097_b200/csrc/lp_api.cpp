@@ -163,9 +163,11 @@ struct EnsembleSpec {
   uint64_t seed = 0;
   DenseMap<int> dmax_by_p;       // depth -> largest D needed
   uint64_t ref_keys = 0;         // distinct (D,P) keys the reference would tally
+  int stage = 0;                 // pipeline stage (pairs ordered by first DP level)
 };
 
 struct Group {
+  int stage = 0;
   int kind = 0;  // 0: register variant, 1: counter variant
   int kmax = 0;
   int threads = 256;
@@ -183,6 +185,14 @@ struct HistPlan {
   std::vector<WorkItem> work;
   std::vector<uint16_t> divtab;
   std::vector<Group> groups;
+  // Pipeline stages: pairs (and so entries, hist rows) are contiguous per
+  // stage, in the order the DP first reads them.
+  struct Stage {
+    int p0 = 0, p1 = 0;      // pairs
+    int e0 = 0, e1 = 0;      // entries
+    int64_t h0 = 0, h1 = 0;  // hist cells
+  };
+  std::vector<Stage> stages;
   int64_t evt_len = 0, h0_len = 0, hist_len = 0;
   uint64_t scenarios = 0, local_scenarios = 0, resolutions = 0, alg_ops = 0;
   int mc_pairs = 0, exact_pairs = 0;
@@ -353,7 +363,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   const uint64_t per_block = std::min<uint64_t>(4096, std::max<uint64_t>(256, ((local_total / want_blocks) + 255) & ~255ull));
 
   // work items, grouped by launch configuration
-  std::map<std::tuple<int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
+  std::map<std::tuple<int, int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
   const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
   const bool legacy = kenv && std::string(kenv) == "legacy";
   const bool inc_off = kenv && std::string(kenv) == "noinc";
@@ -388,7 +398,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           T -= 32;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
-        auto& gv1 = groups[{4, kreg * 16 + wmax, T, sm ? 1 : 0}];
+        auto& gv1 = groups[{specs[pi].stage, 4, kreg * 16 + wmax, T, sm ? 1 : 0}];
         gv1.reserve(gv1.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
@@ -432,7 +442,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T) > kSmemBudgetInc) T >>= 1;
         const size_t smem = smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
-        auto& gv2 = groups[{3, km, T, sm ? 1 : 0}];
+        auto& gv2 = groups[{specs[pi].stage, 3, km, T, sm ? 1 : 0}];
         gv2.reserve(gv2.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
@@ -481,7 +491,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
-        auto& gv3 = groups[{2, kreg, T, sm ? 1 : 0}];
+        auto& gv3 = groups[{specs[pi].stage, 2, kreg, T, sm ? 1 : 0}];
         gv3.reserve(gv3.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
@@ -529,7 +539,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.e_res_hi = e_res;
           w.t0 = t0;
           w.t1 = std::min(pd.t_hi, t0 + kChunkR);
-          groups[{0, km, 256, sm ? 1 : 0}].push_back({w, {smem, 0}});
+          groups[{specs[pi].stage, 0, km, 256, sm ? 1 : 0}].push_back({w, {smem, 0}});
         }
         e = e2;
       }
@@ -554,7 +564,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const bool sm = smem_ctr(e2 - e, pd.k, pd.n, ev, true, T, pmax) <= kSmemBudgetC;
         const size_t smem = smem_ctr(e2 - e, pd.k, pd.n, ev, sm, T, pmax);
         const uint64_t chunk = (uint64_t)T * 8;
-        auto& gv4 = groups[{1, 0, T, sm ? 1 : 0}];
+        auto& gv4 = groups[{specs[pi].stage, 1, 0, T, sm ? 1 : 0}];
         gv4.reserve(gv4.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
         for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
           WorkItem w{};
@@ -574,10 +584,11 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   }
   for (auto& [key, items] : groups) {
     Group g;
-    g.kind = std::get<0>(key);
-    g.kmax = std::get<1>(key);
-    g.threads = std::get<2>(key);
-    g.smem_evt = std::get<3>(key) != 0;
+    g.stage = std::get<0>(key);
+    g.kind = std::get<1>(key);
+    g.kmax = std::get<2>(key);
+    g.threads = std::get<3>(key);
+    g.smem_evt = std::get<4>(key) != 0;
     g.first = (int)hp.work.size();
     g.count = (int)items.size();
     for (auto& it : items) {
@@ -599,6 +610,20 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       g.smem = std::max(g.smem, s);
     }
     hp.groups.push_back(g);
+  }
+  // stage ranges (specs come with non-decreasing stages)
+  int nst = 0;
+  for (const EnsembleSpec& sp : specs) nst = std::max(nst, sp.stage + 1);
+  hp.stages.assign(std::max(nst, 1), HistPlan::Stage{});
+  for (int st = 0, pi = 0; st < (int)hp.stages.size(); ++st) {
+    HistPlan::Stage& S = hp.stages[st];
+    S.p0 = pi;
+    while (pi < (int)specs.size() && specs[pi].stage == st) ++pi;
+    S.p1 = pi;
+    S.e0 = S.p0 < (int)hp.pairs.size() ? hp.pairs[S.p0].entry_base : (int)hp.entries.size();
+    S.e1 = S.p1 < (int)hp.pairs.size() ? hp.pairs[S.p1].entry_base : (int)hp.entries.size();
+    S.h0 = S.e0 < (int)hp.entries.size() ? hp.entries[S.e0].hist_off : hp.hist_len;
+    S.h1 = S.e1 < (int)hp.entries.size() ? hp.entries[S.e1].hist_off : hp.hist_len;
   }
   return LP_OK;
 }
@@ -646,6 +671,34 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   e = launch_finalize((int)hp.pairs.size(), (int)hp.entries.size(), st, d.pairs, d.entries, d.evt,
                       d.h0, d.hist);
   if (!hp.pairs.empty()) *launches += 2;
+  return e;
+}
+
+// The histogram launches of one pipeline stage and its finalize.
+cudaError_t run_hist_stage(const HistPlan& hp, const HistDev& d, cudaStream_t st, int stage,
+                           int* launches) {
+  cudaError_t e = cudaSuccess;
+  for (const Group& g : hp.groups) {
+    if (g.stage != stage) continue;
+    const WorkItem* w = d.work + g.first;
+    if (g.kind == 4)
+      e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+                           d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0);
+    else if (g.kind == 3)
+      e = launch_hist_inc(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w, d.pairs, d.entries,
+                          d.draws, d.binom, d.divtab, d.evt, d.h0);
+    else if (g.kind == 2)
+      e = launch_hist_scn(g.kmax, g.smem_evt, g.count, g.threads, g.smem, g.pmax_cap, st, w, d.pairs,
+                          d.entries, d.draws, d.binom, d.evt, d.h0);
+    else if (g.kind == 0)
+      e = launch_hist_regs(g.kmax, g.smem_evt, g.count, g.smem, st, w, d.pairs, d.entries, d.draws,
+                           d.binom, d.evt, d.h0);
+    else
+      e = launch_hist_ctr(g.smem_evt, g.count, g.threads, g.smem, g.pmax_cap, st, w, d.pairs,
+                          d.entries, d.draws, d.binom, d.evt, d.h0);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+  }
   return e;
 }
 
@@ -710,8 +763,16 @@ struct lp_handle {
   CostScalars cs{};
   int device = 0;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;     // histograms, collectives, fetch (lp_stream)
+  cudaStream_t stream_dp = nullptr;  // DP tables and DP kernels, joined back into `stream`
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kMaxStages = 4;
+  cudaEvent_t ev_stage[kMaxStages] = {};  // probabilities of stage s are in the store
+  cudaStream_t stream_hist[kMaxStages] = {};  // histogram kernels of stage s
+  cudaEvent_t ev_hist[kMaxStages] = {};       // ... done
+  cudaEvent_t ev_start = nullptr;             // scratch cleared for this execute
+  cudaEvent_t ev_join = nullptr;
+  std::vector<int> level_need;  // per DP level: the last stage it must wait for (-1: none)
   std::string err;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -986,12 +1047,18 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
   h->cs = cost_scalars(*costs);
   h->device = device;
   if ((e = cudaSetDevice(device)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&h->stream_dp, cudaStreamNonBlocking)) != cudaSuccess) {
     delete h;
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   for (auto& ev : h->ev_up) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& ev : h->ev_stage) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& ev : h->ev_hist) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& sh : h->stream_hist) cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
   {
     const char* e = getenv("LIVEPUT_DP");
     h->dp_launches = (e && std::string(e) == "launches");
@@ -1010,6 +1077,21 @@ void lp_destroy(lp_handle* h) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : h->ev_up)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->ev_stage)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->ev_hist)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& sh : h->stream_hist)
+    if (sh) {
+      cudaStreamSynchronize(sh);
+      cudaStreamDestroy(sh);
+    }
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->stream_dp) {
+    cudaStreamSynchronize(h->stream_dp);
+    cudaStreamDestroy(h->stream_dp);
+  }
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
@@ -1043,7 +1125,7 @@ Section sec(const std::vector<T>& v, size_t* off) {
 // marks the previous upload out of `pin`, which must finish before the
 // staging memory is rewritten.
 lp_status upload_image(lp_handle* h, std::initializer_list<Section> secs, DevBuf& dst, PinBuf& pin,
-                       cudaEvent_t done, size_t* total) {
+                       cudaEvent_t done, size_t* total, cudaStream_t st) {
   size_t o = 0;
   for (const Section& x : secs) {
     *x.off = o;
@@ -1055,8 +1137,8 @@ lp_status upload_image(lp_handle* h, std::initializer_list<Section> secs, DevBuf
   unsigned char* base = static_cast<unsigned char*>(pin.p);
   for (const Section& x : secs)
     if (x.bytes) std::memcpy(base + *x.off, x.src, x.bytes);
-  LP_CUDA(h, cudaMemcpyAsync(dst.p, pin.p, o, cudaMemcpyHostToDevice, h->stream));
-  LP_CUDA(h, cudaEventRecord(done, h->stream));
+  LP_CUDA(h, cudaMemcpyAsync(dst.p, pin.p, o, cudaMemcpyHostToDevice, st));
+  LP_CUDA(h, cudaEventRecord(done, st));
   *total = o;
   return LP_OK;
 }
@@ -1204,6 +1286,52 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     }
     if (h->store_used + need <= h->cache_max / 8 || pass == 1) break;  // else evict all, retry
   }
+  // Pipeline stages: the fresh ensembles, in the order the DP first reads
+  // them, are cut into up to kMaxStages groups of similar work, so the DP
+  // of the early intervals runs on its own stream while the later
+  // histograms are still being sampled.
+  {
+    static const int want = [] {
+      const char* e = getenv("LIVEPUT_STAGES");
+      const int v = e ? atoi(e) : 3;
+      return std::max(1, std::min(v, (int)lp_handle::kMaxStages));
+    }();
+    uint64_t total = 0, scen = 0;
+    std::vector<uint64_t> cost(fresh.size());
+    for (size_t i = 0; i < fresh.size(); ++i) {
+      const uint64_t local = fresh[i].count / (uint64_t)std::max(h->nranks, 1);
+      cost[i] = alg_ops(local, fresh[i].k, (int)fresh[i].dmax_by_p.size());
+      total += cost[i];
+      scen += local;
+    }
+    const bool staged = want > 1 && fresh.size() >= 2 && scen >= (1u << 18);
+    uint64_t cum = 0;
+    int last = 0;
+    for (size_t i = 0; i < fresh.size(); ++i) {
+      int st = 0;
+      if (staged && total > 0)
+        st = (int)std::min<uint64_t>(want - 1, (uint64_t)want * (cum + cost[i] / 2) / total);
+      st = std::max(st, last);
+      fresh[i].stage = st;
+      last = st;
+      cum += cost[i];
+    }
+    int next_id = -1, prev_raw = -1;  // renumber consecutively
+    for (auto& f : fresh) {
+      if (f.stage != prev_raw) {
+        prev_raw = f.stage;
+        ++next_id;
+      }
+      f.stage = next_id;
+    }
+    h->level_need.assign(H, -1);
+    int need = -1;
+    for (int j = 0; j < H; ++j) {
+      const int si = level_spec[j];
+      if (si >= 0 && fresh_of[si] >= 0) need = std::max(need, fresh[fresh_of[si]].stage);
+      h->level_need[j] = need;
+    }
+  }
   mark("specs");
   std::string err;
   lp_status s = build_hist_plan(fresh, h->rank, h->nranks, h->hp, err, h->num_sms);
@@ -1241,7 +1369,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
                                  sec(h->hp.draws, &h->off_draws), sec(h->hp.binom, &h->off_binom),
                                  sec(h->hp.work, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
                                  sec(h->store_off, &h->off_store_off)},
-                                h->tables, h->pin_up, h->ev_up[0], &bytes);
+                                h->tables, h->pin_up, h->ev_up[0], &bytes, h->stream);
     if (us != LP_OK) return us;
     h->up_bytes = bytes;
   }
@@ -1376,7 +1504,7 @@ lp_status prepare_dp(lp_handle* h) {
                               {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
                                sec(h->pcost, &h->off_cost), sec(h->lrows, &h->off_lrows),
                                sec(h->thr.vals, &h->off_thr), sec(h->thr.row, &h->off_throw)},
-                              h->tables2, h->pin_up2, h->ev_up[1], &bytes);
+                              h->tables2, h->pin_up2, h->ev_up[1], &bytes, h->stream_dp);
   if (us != LP_OK) return us;
   mark("upload2");
   h->up_bytes += bytes;
@@ -1401,29 +1529,60 @@ lp_status exec_hist(lp_handle* h) {
   d.evt = dptr<uint32_t>(h->work, h->w_evt);
   d.h0 = dptr<uint32_t>(h->work, h->w_h0);
   d.hist = dptr<uint32_t>(h->work, h->w_hist);
+  const HistPlan& hp = h->hp;
+  const int nst = (int)hp.stages.size();
+  // one stage + persistent DP: the DP kernel normalises; otherwise each
+  // stage is normalised here and its event releases the DP levels reading it
+  const bool norm_here = nst > 1 || h->dp_launches || h->horizon > kMaxHorizon;
   int launches = 0;
   LP_CUDA(h, cudaEventRecord(h->ev[0], st));
-  LP_CUDA(h, run_hist(h->hp, d, st, &launches));
-  LP_CUDA(h, cudaEventRecord(h->ev[1], st));
-  if (h->nranks > 1 && h->hp.hist_len > 0) {
-    ncclResult_t r = nccl().AllReduce(d.hist, d.hist, (size_t)h->hp.hist_len, ncclUint32, ncclSum,
-                                      h->comm, st);
-    if (r != ncclSuccess) return fail(h, LP_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(r));
+  if (hp.evt_len > 0) LP_CUDA(h, cudaMemsetAsync(d.evt, 0, sizeof(uint32_t) * hp.evt_len, st));
+  LP_CUDA(h, cudaMemsetAsync(d.h0, 0, sizeof(uint32_t) * std::max<int64_t>(hp.h0_len, 1), st));
+  // The stages' histogram kernels go out at once, each on its own stream,
+  // so a stage's tail is filled by the next stage's blocks (the scheduler
+  // favours the earlier launch); finalise / reduce / normalise follow in
+  // stage order on the handle's stream.
+  if (nst > 1) {
+    LP_CUDA(h, cudaEventRecord(h->ev_start, st));
+    for (int s = 0; s < nst; ++s) {
+      LP_CUDA(h, cudaStreamWaitEvent(h->stream_hist[s], h->ev_start, 0));
+      LP_CUDA(h, run_hist_stage(hp, d, h->stream_hist[s], s, &launches));
+      LP_CUDA(h, cudaEventRecord(h->ev_hist[s], h->stream_hist[s]));
+    }
   }
+  for (int s = 0; s < nst; ++s) {
+    const HistPlan::Stage& S = hp.stages[s];
+    if (nst > 1) LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_hist[s], 0));
+    else LP_CUDA(h, run_hist_stage(hp, d, st, s, &launches));
+    LP_CUDA(h, launch_finalize_range(S.p0, S.p1 - S.p0, S.e0, S.e1 - S.e0, st, d.pairs, d.entries, d.evt,
+                                     d.h0, d.hist));
+    if (S.p1 > S.p0) launches += 2;
+    if (s == nst - 1) LP_CUDA(h, cudaEventRecord(h->ev[1], st));
+    if (h->nranks > 1 && S.h1 > S.h0) {
+      ncclResult_t r = nccl().AllReduce(d.hist + S.h0, d.hist + S.h0, (size_t)(S.h1 - S.h0), ncclUint32,
+                                        ncclSum, h->comm, st);
+      if (r != ncclSuccess) return fail(h, LP_ENCCL, "ncclAllReduce: %s", nccl().GetErrorString(r));
+    }
+    if (norm_here && S.e1 > S.e0) {
+      LP_CUDA(h, launch_normalize(S.e1 - S.e0, st, d.pairs, d.entries + S.e0, d.hist,
+                                  dptr<int32_t>(h->tables, h->off_store_off) + S.e0,
+                                  static_cast<double*>(h->store.p)));
+      ++launches;
+    }
+    LP_CUDA(h, cudaEventRecord(h->ev_stage[s], st));
+  }
+  if (nst == 0) LP_CUDA(h, cudaEventRecord(h->ev[1], st));
   LP_CUDA(h, cudaEventRecord(h->ev[2], st));
-  if (h->dp_launches) {
-    LP_CUDA(h, launch_normalize((int)h->hp.entries.size(), st, d.pairs, d.entries, d.hist,
-                                dptr<int32_t>(h->tables, h->off_store_off),
-                                static_cast<double*>(h->store.p)));
-    ++launches;
-  }
   h->stats.kernel_launches = launches;
   return LP_OK;
 }
 
-// execute, part 2: the lookahead DP, traceback and liveput rows.
+// execute, part 2: the lookahead DP and traceback, on the DP stream.  Level
+// j waits only for the stage holding the histograms it reads, so the DP of
+// the early intervals overlaps the sampling of the later ones; the DP
+// stream is joined back into the handle's stream at the end.
 lp_status exec_dp(lp_handle* h) {
-  cudaStream_t st = h->stream;
+  cudaStream_t st = h->stream_dp;
   int launches = 0;
   const LevelDesc* lv = dptr<LevelDesc>(h->tables2, h->off_levels);
   const NodeCfg* cfg = dptr<NodeCfg>(h->tables2, h->off_cfg);
@@ -1436,7 +1595,10 @@ lp_status exec_dp(lp_handle* h) {
   double* stc = dptr<double>(h->work, h->w_stc);
   double* stm = dptr<double>(h->work, h->w_stm);
   double* histp = static_cast<double*>(h->store.p);
-  if (!h->dp_launches && h->horizon <= kMaxHorizon) {
+  const int nst = (int)h->hp.stages.size();
+  const bool persistent = nst <= 1 && !h->dp_launches && h->horizon <= kMaxHorizon;
+  if (persistent) {
+    if (nst == 1) LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[0], 0));
     DpArgs a{};
     a.levels = lv;
     a.cfg = cfg;
@@ -1468,19 +1630,29 @@ lp_status exec_dp(lp_handle* h) {
     LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S));
     ++launches;
   } else {
-  LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
-  LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
-  for (int j = 0; j < h->horizon; ++j) {
-    LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, st, lv, cfg, pcost, histp, thr, throw_,
-                              h->S, val, mig, par, stc, stm));
+    LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
+    LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
+    int waited = -1;
+    for (int j = 0; j < h->horizon; ++j) {
+      const int need = j < (int)h->level_need.size() ? h->level_need[j] : nst - 1;
+      if (need > waited) {
+        LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[need], 0));
+        waited = need;
+      }
+      LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, st, lv, cfg, pcost,
+                                histp, thr, throw_, h->S, val, mig, par, stc, stm));
+      ++launches;
+    }
+    LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
+                               dptr<lp_plan_step>(h->work, h->w_plan),
+                               dptr<double>(h->work, h->w_final)));
     ++launches;
   }
-  LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
-                             dptr<lp_plan_step>(h->work, h->w_plan),
-                             dptr<double>(h->work, h->w_final)));
-  ++launches;
-  }
+  // every stage has landed in the store before the handle's stream moves on
+  if (nst > 0) LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[nst - 1], 0));
   LP_CUDA(h, cudaEventRecord(h->ev[3], st));
+  LP_CUDA(h, cudaEventRecord(h->ev_join, st));
+  LP_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   h->live_pending = !h->lrows.empty();  // the liveput table is built on demand (lp_fetch)
   h->stats.kernel_launches += launches;
   return LP_OK;

@@ -392,6 +392,20 @@ cudaError_t launch_hist_ctr(bool smem_evt, int blocks, int threads, size_t smem,
   return cudaGetLastError();
 }
 
+// Finalize of a stage: pairs [p0, p0 + n_pairs), entries [e0, e0 + n_entries).
+cudaError_t launch_finalize_range(int p0, int n_pairs, int e0, int n_entries, cudaStream_t st,
+                                  const PairDesc* pairs, const EntryDesc* ents, uint32_t* evt,
+                                  uint32_t* h0, uint32_t* hist) {
+  if (n_pairs > 0) {
+    h0_scan_kernel<<<n_pairs, 32, 0, st>>>(pairs + p0, h0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (n_entries <= 0) return cudaSuccess;
+  finalize_kernel<<<n_entries, 128, 0, st>>>(pairs, ents + e0, evt, h0, hist);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(int n_pairs, int n_entries, cudaStream_t st, const PairDesc* pairs,
                             const EntryDesc* ents, uint32_t* evt, uint32_t* h0, uint32_t* hist) {
   if (n_pairs <= 0) return cudaSuccess;

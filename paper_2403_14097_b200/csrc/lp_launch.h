@@ -28,6 +28,9 @@ cudaError_t launch_hist_rows(int kreg, int wmax, bool smem_evt, int blocks, int 
                              size_t smem, cudaStream_t st, const WorkItem* w,
                              const PairDesc* pairs, const EntryDesc* ents, const DrawConst* dr,
                              const uint64_t* binom, uint32_t* evt, uint32_t* h0);
+cudaError_t launch_finalize_range(int p0, int n_pairs, int e0, int n_entries, cudaStream_t st,
+                                  const PairDesc* pairs, const EntryDesc* ents, uint32_t* evt,
+                                  uint32_t* h0, uint32_t* hist);
 cudaError_t launch_finalize(int n_pairs, int n_entries, cudaStream_t st, const PairDesc* pairs,
                             const EntryDesc* ents, uint32_t* evt, uint32_t* h0, uint32_t* hist);
 cudaError_t launch_dump(int n, int k, int exact, int trials, uint64_t seed, const DrawConst* dc,
