@@ -226,6 +226,45 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
   return o;
 }
 
+// phi of two depth-changing pairs (prev a, prev b -> the same next,
+// non-strict) with their bin loops interleaved: two independent FP64 chains
+// per step instead of one.  Each pair's operation sequence is exactly
+// phi_dev's fast path (bins d = dmax .. 0 in order, +0.0 past d = 0).
+__device__ __forceinline__ void phi_fast2(const NodeCfg& a, const NodeCfg& b, const double* ha,
+                                          const double* hb, int k, double rate, const PhiConst& K,
+                                          PhiOut& oa, PhiOut& ob) {
+  const int da = min(k, a.d), db = min(k, b.d);
+  double ca, ma, cb, mb;
+  {  // bin d = dmax: the rollback bin (m = 0) when every assigned slot can be lost
+    const double pa = ha[da], pb = hb[db];
+    const bool ra = da == a.d, rb = db == b.d;
+    ca = __dadd_rn(0.0, __dmul_rn(__dmul_rn(pa, rate), ra ? K.teff_rb : K.teff_pipe));
+    ma = __dadd_rn(0.0, __dmul_rn(pa, ra ? K.c_rb : K.c_pipe));
+    cb = __dadd_rn(0.0, __dmul_rn(__dmul_rn(pb, rate), rb ? K.teff_rb : K.teff_pipe));
+    mb = __dadd_rn(0.0, __dmul_rn(pb, rb ? K.c_rb : K.c_pipe));
+  }
+  const int nb = max(da, db);  // bins i = 1 .. nb (d = dmax - i)
+  for (int i0 = 1; i0 <= nb; i0 += 8) {
+    double pa[8], pb[8];
+    const double* qa = ha + (da - i0);
+    const double* qb = hb + (db - i0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      pa[u] = (i0 + u <= da) ? qa[-u] : 0.0;
+      pb[u] = (i0 + u <= db) ? qb[-u] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      ca = __dadd_rn(ca, __dmul_rn(__dmul_rn(pa[u], rate), K.teff_pipe));
+      cb = __dadd_rn(cb, __dmul_rn(__dmul_rn(pb[u], rate), K.teff_pipe));
+      ma = __dadd_rn(ma, __dmul_rn(pa[u], K.c_pipe));
+      mb = __dadd_rn(mb, __dmul_rn(pb[u], K.c_pipe));
+    }
+  }
+  oa = PhiOut{ca, ma};
+  ob = PhiOut{cb, mb};
+}
+
 // hist[m] = count_m / count, once per re-plan (after the cross-rank reduce),
 // so the DP's inner loop has no FP64 division.  One block per depth entry.
 __global__ void normalize_kernel(const PairDesc* __restrict__ pairs,
@@ -300,20 +339,46 @@ __global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __
   }
   const PhiConst K = phi_const(L, S, nc);
   Cand best{0.0, 0.0, 0.0, 0.0, -1};
-  for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
-    const int gi = L.prev_base + pi;
-    const NodeCfg pv = cfg[gi];
-    const double* hp = histp + pv.hist_off;
-    const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{hp}, thr_tab, thr_row, K);
+  // full take-order key (value desc, mig asc, index asc): prevs may be
+  // folded out of index order below
+  auto take = [&](int pi, int gi, const PhiOut& ph) {
     const double v = __dadd_rn(val[gi], ph.committed);
     const double mg = __dadd_rn(mig[gi], ph.mig);
-    if (best.idx < 0 || v > best.value || (v == best.value && mg < best.mig)) {
+    if (best.idx < 0 || v > best.value ||
+        (v == best.value && (mg < best.mig || (mg == best.mig && pi < best.idx)))) {
       best.value = v;
       best.mig = mg;
       best.stc = ph.committed;
       best.stm = ph.mig;
       best.idx = pi;
     }
+  };
+  // depth-changing prevs (most of them) are evaluated two at a time
+  const bool fast_ok = nx.d > 0 && !S.strict;
+  int held = -1;  // an eligible prev waiting for a partner
+  NodeCfg held_cfg{};
+  for (int pi = threadIdx.x; pi < L.prev_count; pi += blockDim.x) {
+    const int gi = L.prev_base + pi;
+    const NodeCfg pv = cfg[gi];
+    if (fast_ok && pv.d > 0 && pv.p != nx.p) {
+      if (held < 0) {
+        held = pi;
+        held_cfg = pv;
+        continue;
+      }
+      PhiOut oa, ob;
+      phi_fast2(held_cfg, pv, histp + held_cfg.hist_off, histp + pv.hist_off, L.k, nc.thr, K, oa, ob);
+      take(held, L.prev_base + held, oa);
+      take(pi, gi, ob);
+      held = -1;
+      continue;
+    }
+    const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{histp + pv.hist_off}, thr_tab, thr_row, K);
+    take(pi, gi, ph);
+  }
+  if (held >= 0) {
+    const PhiOut ph = phi_dev(held_cfg, nx, nc, L, S, ProbPtr{histp + held_cfg.hist_off}, thr_tab, thr_row, K);
+    take(held, L.prev_base + held, ph);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
