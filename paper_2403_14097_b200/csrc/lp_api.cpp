@@ -768,7 +768,7 @@ struct lp_handle {
   cudaStream_t stream = nullptr;     // histograms, collectives, fetch (lp_stream)
   cudaStream_t stream_dp = nullptr;  // DP tables and DP kernels, joined back into `stream`
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  static constexpr int kMaxStages = 4;
+  static constexpr int kMaxStages = 16;
   cudaEvent_t ev_stage[kMaxStages] = {};  // probabilities of stage s are in the store
   cudaStream_t stream_hist[kMaxStages] = {};  // histogram kernels of stage s
   cudaEvent_t ev_hist[kMaxStages] = {};       // ... done
@@ -1293,11 +1293,13 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   // of the early intervals runs on its own stream while the later
   // histograms are still being sampled.
   {
-    static const int want = [] {
+    // LIVEPUT_STAGES = 1..4: shrinking cost cuts; 0: one stage per ensemble
+    static const int want_env = [] {
       const char* e = getenv("LIVEPUT_STAGES");
-      const int v = e ? atoi(e) : 3;
-      return std::max(1, std::min(v, (int)lp_handle::kMaxStages));
+      return e ? atoi(e) : 3;
     }();
+    const int want = want_env == 0 ? std::min((int)fresh.size(), (int)lp_handle::kMaxStages)
+                                   : std::max(1, std::min(want_env, 4));
     uint64_t total = 0, scen = 0;
     std::vector<uint64_t> cost(fresh.size());
     for (size_t i = 0; i < fresh.size(); ++i) {
@@ -1314,8 +1316,12 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     for (size_t i = 0; i < fresh.size(); ++i) {
       int st = 0;
       if (staged && total > 0) {
-        const double mid = (static_cast<double>(cum) + 0.5 * static_cast<double>(cost[i])) / static_cast<double>(total);
-        while (st < want - 1 && mid > kCuts[want - 1][st]) ++st;
+        if (want_env == 0) {
+          st = (int)std::min<size_t>(i, want - 1);
+        } else {
+          const double mid = (static_cast<double>(cum) + 0.5 * static_cast<double>(cost[i])) / static_cast<double>(total);
+          while (st < want - 1 && mid > kCuts[want - 1][st]) ++st;
+        }
       }
       st = std::max(st, last);
       fresh[i].stage = st;
