@@ -1,0 +1,49 @@
+"""The execution modes of a re-plan must not change its result: one stage with
+the persistent DP kernel, three pipelined stages with per-level DP launches,
+one stage per ensemble, and the per-level launches alone all give the same
+plan (configs and FP64 step values, bit for bit).  The mode switches are read
+once per process, so each mode runs in a subprocess."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+SCRIPT = r"""
+import json, sys
+sys.path.insert(0, %r)
+from bench import north_star_nseq
+from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_1p5b, lm_6p7b
+from paper_2403_14097_b200.planner import Planner, reactive_plan
+out = []
+for w, ns, trials in [(lm_1p5b(), north_star_nseq(256, 24), 300000),
+                      (lm_6p7b(), [128, 120, 121, 110, 118, 104, 104, 96, 100, 90, 97], 200000),
+                      (lm_1p5b(), [77, 70, 71, 64, 69, 60], 50000)]:
+    p = Planner(w, CostTable(), PlannerOptions(mc_trials=trials))
+    plan = p.dp_optimize(reactive_plan(ns[0], w), ns, want_liveput=True)
+    out.append([[s.config.pipelines if s.config else 0, s.config.stages if s.config else 0,
+                 s.expected_committed.hex(), s.expected_mig_cost_s.hex()] for s in plan])
+    out.append([[r.interval, r.liveput.hex()] for r in p.last_liveput[:50]])
+    p.close()
+print(json.dumps(out))
+""" % str(ROOT)
+
+
+def _run(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.gpu
+def test_execution_modes_agree():
+    base = _run({"LIVEPUT_STAGES": "1"})  # one stage: persistent cooperative DP
+    for env in ({"LIVEPUT_STAGES": "3"}, {"LIVEPUT_STAGES": "0"},
+                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"}):
+        assert _run(env) == base, env
