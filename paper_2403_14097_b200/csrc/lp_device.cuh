@@ -155,7 +155,7 @@ __device__ __forceinline__ uint32_t gen_mc_bitmap_smem(uint64_t seed, uint64_t t
     }
     const uint32_t sel = (j == static_cast<uint32_t>(i)) ? vi : vj;
     map[i * ms] = (j << 16) | vi;
-    BMc[(sel >> 5) * T] |= 1u << (sel & 31);
+    atomicOr(BMc + (sel >> 5) * T, 1u << (sel & 31));
     smin = min(smin, sel);
   }
   return smin;
@@ -190,7 +190,9 @@ __device__ __forceinline__ uint32_t gen_mc_bitmap_tab(uint64_t seed, uint64_t t,
     const uint32_t sel = (j == ui) ? vi : vj;
     TAB[oj] = static_cast<uint8_t>(vi);  // position j now holds the old pool[i]
     *dw = dj | (1u << (j & 31u));
-    BMc[(sel >> 5) * T] |= 1u << (sel & 31u);
+    // fire-and-forget OR: the column is this thread's, but a shared-memory
+    // atomic has no result to wait for, so the next draw does not stall on it
+    atomicOr(BMc + (sel >> 5) * T, 1u << (sel & 31u));
     smin = min(smin, sel);
   }
   return smin;

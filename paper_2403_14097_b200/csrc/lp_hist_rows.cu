@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __res
       else gen_mc_regs<KS>(pd.seed, t, k, dc, sl);
 #pragma unroll
       for (int i = 0; i < KS; ++i)
-        if (sl[i] != 0xffffffffu) BMc[(sl[i] >> 5) * T] |= 1u << (sl[i] & 31);
+        if (sl[i] != 0xffffffffu) atomicOr(BMc + (sl[i] >> 5) * T, 1u << (sl[i] & 31));
       s0 = sl[0];
     } else if (pd.exact) {
       uint64_t rank = t;
