@@ -1166,6 +1166,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->prepared = false;  // until prepare_dp has run
   if (!n_seq || len < 2) return fail(h, LP_EINVAL, "dp_optimize: need at least N_i and N_{i+1}");
   cudaSetDevice(h->device);
+  mark("setdev");
   for (int i = 0; i < len; ++i) {
     if (n_seq[i] < 0) return fail(h, LP_EINVAL, "dp_optimize: negative availability");
     if (n_seq[i] > kMaxN)
@@ -1188,6 +1189,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     h->cfg.reserve(total);
   }
   std::vector<int> lbase(H + 1), lcount(H + 1);
+  mark("reserve");
   // level 0: current
   lbase[0] = 0;
   lcount[0] = 1;
