@@ -318,6 +318,77 @@ lp_status lp_predict_windows(const int32_t* counts, int32_t len, const lp_foreca
  * when actual sums to zero and pred does not. */
 double lp_eval_l1(const int32_t* pred, const int32_t* actual, int32_t len);
 
+/* ---- the replay driver: the reference simulator's run()
+ *      (simulator.cpp:119-340) over an availability trace, with this
+ *      library's planner (its device histogram store persists across the
+ *      re-plans) and forecasts.  Host bookkeeping (placements, rollbacks,
+ *      sample accounting, the ledger) restates the reference exactly. ---- */
+typedef enum {
+  LP_POLICY_PROACTIVE = 0, /* PolicyKind (simulator.hpp:16-22) */
+  LP_POLICY_IDEAL = 1,
+  LP_POLICY_REACTIVE = 2,
+  LP_POLICY_CHECKPOINT = 3,
+  LP_POLICY_REDUNDANCY = 4
+} lp_policy_kind;
+
+/* Policy (simulator.hpp:38-75) with CheckpointParams / RedundancyParams. */
+typedef struct {
+  int32_t kind;
+  int32_t lookahead;       /* proactive / ideal */
+  int32_t method;          /* proactive: lp_predict_method */
+  int32_t history;         /* proactive */
+  int32_t ckpt_period_intervals;
+  int32_t redundancy_fixed_stages;
+  double ckpt_save_cost_s;
+  double ckpt_restore_cost_s;
+  double ckpt_restart_cost_s;
+  double redundancy_slowdown;
+} lp_policy;
+
+/* Ledger (simulator.hpp:85-97): instance-seconds by category. */
+typedef struct {
+  double effective_s, migration_s, checkpoint_s, wasted_rollback_s, idle_s;
+} lp_ledger;
+
+/* IntervalLog (simulator.hpp:99-109). */
+typedef struct {
+  int32_t interval, available, pipelines, stages;
+  double throughput;
+  int64_t committed, rolled_back;
+  int32_t migration; /* lp_migration_kind */
+  int32_t pad;
+  lp_ledger ledger;
+} lp_interval_log;
+
+/* SimReport (simulator.hpp:111-127) without the per-interval vector. */
+typedef struct {
+  uint64_t seed;
+  int64_t committed_samples;
+  double wall_time_s;
+  lp_ledger ledger;
+  double instance_seconds, instance_hours, spot_cost, ondemand_cost;
+  double cost_per_sample; /* valid when has_cost_per_sample */
+  int32_t has_cost_per_sample;
+  int32_t epochs_completed, rollback_events, suspended_intervals, sample_accounting_ok;
+  int32_t pad;
+} lp_sim_report;
+
+/* The reference's defaults: Policy::Proactive(12, arima, 12),
+ * CheckpointParams{5, 10, 30, 30}, RedundancyParams{4, 0.75}. */
+lp_policy lp_policy_defaults(int32_t kind);
+/* run(series, w, policy, seed, {epoch_samples, planner, costs}, shared):
+ * counts[0 .. len) at interval_s seconds, capacity for the forecasts.
+ * shared != NULL: plan with that handle as is (the reference's injected
+ * Planner); else a private planner from (profile, costs, planner options)
+ * with interval_s = interval_s and rollback = the policy's restore cost, on
+ * `device`.  logs: len entries.  spot / on-demand prices per instance-hour
+ * (WorkloadProfile::spot_price_per_hour etc.). */
+lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
+                      const lp_options* planner_options, int32_t device, const int32_t* counts,
+                      int32_t len, double interval_s, int32_t capacity, const lp_policy* policy,
+                      uint64_t seed, int32_t epoch_samples, double spot_price_per_hour,
+                      double ondemand_price_per_hour, lp_sim_report* report, lp_interval_log* logs);
+
 /* Build information (sm arch, sizes supported). */
 int32_t lp_max_instances(void);
 const char* lp_build_info(void);

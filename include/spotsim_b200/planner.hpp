@@ -43,6 +43,8 @@ struct WorkloadProfile {
   double alpha_s = 0.0;
   double beta_s_per_byte = 0.0;
   std::map<int, double> pipeline_rates;
+  double spot_price_per_hour = 0.0;      // simulator costs only
+  double ondemand_price_per_hour = 0.0;
 };
 
 struct CostTable {
@@ -357,6 +359,145 @@ inline double resume_cost(const ParallelConfig& target, const WorkloadProfile& w
   detail::ProfileC p(w);
   const lp_costs c = detail::to_c(costs);
   return lp_resume_cost(&p.p, &c, {target.pipelines, target.stages});
+}
+
+// ---- simulator.hpp:14-140 — the replay driver over this planner ---------
+struct IntervalSeries {  // trace.hpp:17-24
+  double interval_seconds = 60.0;
+  int capacity = 0;
+  std::vector<int> counts;
+};
+
+enum class PolicyKind { proactive, ideal, reactive, checkpoint, redundancy };
+enum class PredictMethod { arima, moving_avg, exp_smooth, last_value };
+
+struct CheckpointParams {
+  int period_intervals = 5;
+  double save_cost_s = 10.0, restore_cost_s = 30.0, restart_cost_s = 30.0;
+};
+struct RedundancyParams {
+  int fixed_stages = 4;
+  double slowdown_factor = 0.75;
+};
+struct Policy {
+  PolicyKind kind = PolicyKind::reactive;
+  int lookahead = 12;
+  PredictMethod method = PredictMethod::arima;
+  int history = 12;
+  CheckpointParams checkpoint;
+  RedundancyParams redundancy;
+  static Policy Proactive(int lookahead = 12, PredictMethod m = PredictMethod::arima, int history = 12) {
+    Policy p;
+    p.kind = PolicyKind::proactive;
+    p.lookahead = lookahead;
+    p.method = m;
+    p.history = history;
+    return p;
+  }
+  static Policy Ideal(int lookahead = 12) {
+    Policy p;
+    p.kind = PolicyKind::ideal;
+    p.lookahead = lookahead;
+    return p;
+  }
+  static Policy Reactive() { return Policy{}; }
+  static Policy Checkpoint(CheckpointParams c = {}) {
+    Policy p;
+    p.kind = PolicyKind::checkpoint;
+    p.checkpoint = c;
+    return p;
+  }
+  static Policy Redundancy(int fixed_stages, double slowdown = 0.75) {
+    Policy p;
+    p.kind = PolicyKind::redundancy;
+    p.redundancy = {fixed_stages, slowdown};
+    return p;
+  }
+};
+
+struct SimOptions {
+  int epoch_samples = 0;
+  PlannerOptions planner;
+  CostTable costs;
+};
+
+struct Ledger {
+  double effective_s = 0.0, migration_s = 0.0, checkpoint_s = 0.0, wasted_rollback_s = 0.0, idle_s = 0.0;
+  double total() const { return effective_s + migration_s + checkpoint_s + wasted_rollback_s + idle_s; }
+};
+
+struct IntervalLog {
+  int interval = 0, available = 0, pipelines = 0, stages = 0;
+  double throughput = 0.0;
+  long long committed = 0, rolled_back = 0;
+  MigrationKind migration = MigrationKind::none;
+  Ledger ledger;
+};
+
+struct SimReport {
+  std::string policy;
+  uint64_t seed = 0;
+  std::vector<IntervalLog> intervals;
+  long long committed_samples = 0;
+  double wall_time_s = 0.0;
+  Ledger ledger;
+  double instance_seconds = 0.0, instance_hours = 0.0, spot_cost = 0.0, ondemand_cost = 0.0;
+  std::optional<double> cost_per_sample;
+  int epochs_completed = 0, rollback_events = 0, suspended_intervals = 0;
+  bool sample_accounting_ok = true;
+};
+
+// run (simulator.cpp:119-340); the planner is `shared` when given, else a
+// private one on `device`.
+inline SimReport run(const IntervalSeries& series, const WorkloadProfile& w, const Policy& policy,
+                     uint64_t seed, const SimOptions& options = {}, Planner* shared = nullptr,
+                     int device = 0) {
+  detail::ProfileC p(w);
+  const lp_costs c = detail::to_c(options.costs);
+  const lp_options o = detail::to_c(options.planner);
+  lp_policy pol = lp_policy_defaults(static_cast<int32_t>(policy.kind));
+  pol.lookahead = policy.lookahead;
+  pol.method = static_cast<int32_t>(policy.method);
+  pol.history = policy.history;
+  pol.ckpt_period_intervals = policy.checkpoint.period_intervals;
+  pol.ckpt_save_cost_s = policy.checkpoint.save_cost_s;
+  pol.ckpt_restore_cost_s = policy.checkpoint.restore_cost_s;
+  pol.ckpt_restart_cost_s = policy.checkpoint.restart_cost_s;
+  pol.redundancy_fixed_stages = policy.redundancy.fixed_stages;
+  pol.redundancy_slowdown = policy.redundancy.slowdown_factor;
+  std::vector<lp_interval_log> logs(series.counts.size() + 1);
+  lp_sim_report r{};
+  std::vector<int32_t> counts(series.counts.begin(), series.counts.end());
+  detail::check(lp_simulate(shared ? shared->handle() : nullptr, &p.p, &c, &o, device, counts.data(),
+                            static_cast<int32_t>(counts.size()), series.interval_seconds, series.capacity,
+                            &pol, seed, options.epoch_samples, w.spot_price_per_hour,
+                            w.ondemand_price_per_hour, &r, logs.data()),
+                nullptr);
+  static const char* kNames[] = {"proactive", "ideal", "reactive", "checkpoint", "redundancy"};
+  SimReport rep;
+  rep.policy = kNames[static_cast<int>(policy.kind)];
+  rep.seed = r.seed;
+  rep.committed_samples = r.committed_samples;
+  rep.wall_time_s = r.wall_time_s;
+  auto led = [](const lp_ledger& l) {
+    return Ledger{l.effective_s, l.migration_s, l.checkpoint_s, l.wasted_rollback_s, l.idle_s};
+  };
+  rep.ledger = led(r.ledger);
+  rep.instance_seconds = r.instance_seconds;
+  rep.instance_hours = r.instance_hours;
+  rep.spot_cost = r.spot_cost;
+  rep.ondemand_cost = r.ondemand_cost;
+  if (r.has_cost_per_sample) rep.cost_per_sample = r.cost_per_sample;
+  rep.epochs_completed = r.epochs_completed;
+  rep.rollback_events = r.rollback_events;
+  rep.suspended_intervals = r.suspended_intervals;
+  rep.sample_accounting_ok = r.sample_accounting_ok != 0;
+  for (size_t i = 0; i < series.counts.size(); ++i) {
+    const lp_interval_log& L = logs[i];
+    rep.intervals.push_back({L.interval, L.available, L.pipelines, L.stages, L.throughput, L.committed,
+                             L.rolled_back, static_cast<MigrationKind>(L.migration), led(L.ledger)});
+  }
+  return rep;
 }
 
 }  // namespace spotsim_b200

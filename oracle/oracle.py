@@ -123,6 +123,9 @@ def ref_lib():
             "ref_resume_cost": (C.c_double, [C.c_int, C.c_int, prof, costs]),
             "ref_predict": (C.c_int, [_P(C.c_int), C.c_int, _P(C.c_int), _P(C.c_double), C.c_int, _P(C.c_int)]),
             "ref_eval_l1": (C.c_double, [_P(C.c_int), _P(C.c_int), C.c_int]),
+            "ref_simulate": (C.c_int, [_P(C.c_int), C.c_int, C.c_double, C.c_int, prof, C.c_double, C.c_double, costs,
+                                       opts, _P(C.c_int), _P(C.c_double), C.c_uint64, C.c_int, _P(C.c_double),
+                                       _P(C.c_int), _P(C.c_longlong), _P(C.c_double)]),
             "ref_plan_migration": (C.c_int, [C.c_int] * 3 + [_P(C.c_uint8), C.c_int, C.c_int, C.c_int, prof, costs,
                                              _P(C.c_int), _P(C.c_int), C.c_int, _P(C.c_double)]),
             "ref_gen_synthetic": (C.c_int, [C.c_uint64] + [C.c_int] * 6 + [_P(C.c_int), C.c_int]),
@@ -383,3 +386,39 @@ def ref_gen_synthetic(seed, cap, length, loss_events, gain_events, min_step, max
     out = (C.c_int * (length + 8))()
     n = l.ref_gen_synthetic(seed, cap, length, loss_events, gain_events, min_step, max_step, out, length + 8)
     return list(out[:n])
+
+
+def ref_simulate(counts, w, pol, seed, opt, costs, interval_s=60.0, capacity=0, epoch_samples=0, spot=0.0,
+                 ondemand=0.0):
+    """The reference's run() through oracle/_ref; same dict layout as
+    paper_2403_14097_b200.planner.simulate."""
+    import math
+    l = ref_lib()
+    p, keep = w.to_c()
+    c = costs.to_c()
+    o = opt.to_c()
+    n = len(counts)
+    cnt = (C.c_int * max(n, 1))(*counts)
+    pi = (C.c_int * 6)(pol.kind, pol.lookahead, pol.method, pol.history, pol.ckpt_period_intervals,
+                       pol.redundancy_fixed_stages)
+    pd = (C.c_double * 4)(pol.ckpt_save_cost_s, pol.ckpt_restore_cost_s, pol.ckpt_restart_cost_s,
+                          pol.redundancy_slowdown)
+    rd = (C.c_double * 12)()
+    ri = (C.c_int * 4)()
+    li = (C.c_longlong * (7 * max(n, 1)))()
+    ld = (C.c_double * (6 * max(n, 1)))()
+    rc = l.ref_simulate(cnt, n, interval_s, capacity, C.byref(p), spot, ondemand, C.byref(c), C.byref(o), pi, pd,
+                        seed, epoch_samples, rd, ri, li, ld)
+    if rc != 0:
+        raise ValueError(l.ref_last_error().decode())
+    led = lambda a: {"effective_s": a[0], "migration_s": a[1], "checkpoint_s": a[2], "wasted_rollback_s": a[3],
+                     "idle_s": a[4]}
+    report = {"seed": seed, "committed_samples": int(rd[0]), "wall_time_s": rd[1], "ledger": led(rd[2:7]),
+              "instance_seconds": rd[7], "instance_hours": rd[8], "spot_cost": rd[9], "ondemand_cost": rd[10],
+              "cost_per_sample": None if math.isnan(rd[11]) else rd[11], "epochs_completed": ri[0],
+              "rollback_events": ri[1], "suspended_intervals": ri[2], "sample_accounting_ok": bool(ri[3])}
+    names = ["none", "intra_stage", "inter_stage", "pipeline"]
+    ivs = [{"interval": li[7 * i], "available": li[7 * i + 1], "pipelines": li[7 * i + 2], "stages": li[7 * i + 3],
+            "throughput": ld[6 * i], "committed": li[7 * i + 4], "rolled_back": li[7 * i + 5],
+            "migration": names[li[7 * i + 6]], "ledger": led(ld[6 * i + 1: 6 * i + 6])} for i in range(n)]
+    return report, ivs

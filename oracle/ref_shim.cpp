@@ -15,6 +15,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <limits>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -30,6 +31,7 @@
 #include "spotsim/rng.hpp"
 #include "spotsim/trace.hpp"
 #include "spotsim/predictor.hpp"
+#include "spotsim/simulator.hpp"
 
 #include "liveput.h"
 
@@ -338,6 +340,83 @@ double ref_eval_l1(const int* pred, const int* actual, int len) {
   Forecast f;
   f.values.assign(pred, pred + len);
   return eval_l1(f, std::vector<int>(actual, actual + len));
+}
+
+// run() (simulator.cpp:119-340).  pol_i = {kind, lookahead, method, history,
+// ckpt_period, redundancy_stages}, pol_d = {save, restore, restart,
+// slowdown}.  rep_d = {committed_samples, wall_time_s, ledger x5,
+// instance_seconds, instance_hours, spot_cost, ondemand_cost,
+// cost_per_sample (NaN if none)}, rep_i = {epochs_completed,
+// rollback_events, suspended_intervals, sample_accounting_ok}.
+// log_i: 7 per interval {interval, available, pipelines, stages, committed,
+// rolled_back, migration}; log_d: 6 per interval {throughput, ledger x5}.
+int ref_simulate(const int* counts, int len, double interval_s, int capacity, const lp_profile* p,
+                 double spot, double ondemand, const lp_costs* c, const lp_options* o, const int* pol_i,
+                 const double* pol_d, uint64_t seed, int epoch_samples, double* rep_d, int* rep_i,
+                 long long* log_i, double* log_d) {
+  try {
+    IntervalSeries series;
+    series.interval_seconds = interval_s;
+    series.capacity = capacity;
+    series.counts.assign(counts, counts + len);
+    WorkloadProfile w = to_profile(p);
+    w.spot_price_per_hour = spot;
+    w.ondemand_price_per_hour = ondemand;
+    Policy pol;
+    pol.kind = (PolicyKind)pol_i[0];
+    pol.lookahead = pol_i[1];
+    pol.method = (PredictMethod)pol_i[2];
+    pol.history = pol_i[3];
+    pol.checkpoint.period_intervals = pol_i[4];
+    pol.redundancy.fixed_stages = pol_i[5];
+    pol.checkpoint.save_cost_s = pol_d[0];
+    pol.checkpoint.restore_cost_s = pol_d[1];
+    pol.checkpoint.restart_cost_s = pol_d[2];
+    pol.redundancy.slowdown_factor = pol_d[3];
+    SimOptions so;
+    so.epoch_samples = epoch_samples;
+    so.planner = to_options(o);
+    so.costs = to_costs(c);
+    SimReport r = run(series, w, pol, seed, so, nullptr);
+    rep_d[0] = (double)r.committed_samples;
+    rep_d[1] = r.wall_time_s;
+    rep_d[2] = r.ledger.effective_s;
+    rep_d[3] = r.ledger.migration_s;
+    rep_d[4] = r.ledger.checkpoint_s;
+    rep_d[5] = r.ledger.wasted_rollback_s;
+    rep_d[6] = r.ledger.idle_s;
+    rep_d[7] = r.instance_seconds;
+    rep_d[8] = r.instance_hours;
+    rep_d[9] = r.spot_cost;
+    rep_d[10] = r.ondemand_cost;
+    rep_d[11] = r.cost_per_sample ? *r.cost_per_sample : std::numeric_limits<double>::quiet_NaN();
+    rep_i[0] = r.epochs_completed;
+    rep_i[1] = r.rollback_events;
+    rep_i[2] = r.suspended_intervals;
+    rep_i[3] = r.sample_accounting_ok ? 1 : 0;
+    for (int i = 0; i < len; ++i) {
+      const IntervalLog& L = r.intervals[i];
+      long long* li = log_i + 7 * i;
+      li[0] = L.interval;
+      li[1] = L.available;
+      li[2] = L.pipelines;
+      li[3] = L.stages;
+      li[4] = L.committed;
+      li[5] = L.rolled_back;
+      li[6] = (long long)L.migration;
+      double* ld = log_d + 6 * i;
+      ld[0] = L.throughput;
+      ld[1] = L.ledger.effective_s;
+      ld[2] = L.ledger.migration_s;
+      ld[3] = L.ledger.checkpoint_s;
+      ld[4] = L.ledger.wasted_rollback_s;
+      ld[5] = L.ledger.idle_s;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
 }
 
 // gen_synthetic (trace.cpp:80-180): writes up to cap counts, returns length.

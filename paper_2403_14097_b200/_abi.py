@@ -16,6 +16,7 @@ LIB_PATH = PKG_DIR / "lib" / "libliveput.so"
 LP_OK, LP_EINVAL, LP_ECUDA, LP_ENOMEM, LP_EUNSUPPORTED, LP_ENCCL, LP_EROLLBACK = range(7)
 LP_MIG_NONE, LP_MIG_INTRA_STAGE, LP_MIG_INTER_STAGE, LP_MIG_PIPELINE = range(4)
 LP_PREDICT_ARIMA, LP_PREDICT_MOVING_AVG, LP_PREDICT_EXP_SMOOTH, LP_PREDICT_LAST_VALUE = range(4)
+LP_POLICY_PROACTIVE, LP_POLICY_IDEAL, LP_POLICY_REACTIVE, LP_POLICY_CHECKPOINT, LP_POLICY_REDUNDANCY = range(5)
 LP_NCCL_ID_BYTES = 128
 
 
@@ -116,6 +117,33 @@ class lp_forecast_config(C.Structure):
                 ("steep_decay", C.c_double)]
 
 
+class lp_policy(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lookahead", C.c_int32), ("method", C.c_int32), ("history", C.c_int32),
+                ("ckpt_period_intervals", C.c_int32), ("redundancy_fixed_stages", C.c_int32),
+                ("ckpt_save_cost_s", C.c_double), ("ckpt_restore_cost_s", C.c_double),
+                ("ckpt_restart_cost_s", C.c_double), ("redundancy_slowdown", C.c_double)]
+
+
+class lp_ledger(C.Structure):
+    _fields_ = [("effective_s", C.c_double), ("migration_s", C.c_double), ("checkpoint_s", C.c_double),
+                ("wasted_rollback_s", C.c_double), ("idle_s", C.c_double)]
+
+
+class lp_interval_log(C.Structure):
+    _fields_ = [("interval", C.c_int32), ("available", C.c_int32), ("pipelines", C.c_int32),
+                ("stages", C.c_int32), ("throughput", C.c_double), ("committed", C.c_int64),
+                ("rolled_back", C.c_int64), ("migration", C.c_int32), ("pad", C.c_int32), ("ledger", lp_ledger)]
+
+
+class lp_sim_report(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("committed_samples", C.c_int64), ("wall_time_s", C.c_double),
+                ("ledger", lp_ledger), ("instance_seconds", C.c_double), ("instance_hours", C.c_double),
+                ("spot_cost", C.c_double), ("ondemand_cost", C.c_double), ("cost_per_sample", C.c_double),
+                ("has_cost_per_sample", C.c_int32), ("epochs_completed", C.c_int32),
+                ("rollback_events", C.c_int32), ("suspended_intervals", C.c_int32),
+                ("sample_accounting_ok", C.c_int32), ("pad", C.c_int32)]
+
+
 class LiveputError(RuntimeError):
     pass
 
@@ -172,6 +200,10 @@ _SIGS = {
     "lp_predict_windows": (C.c_int, [_P(C.c_int32), C.c_int32, _P(lp_forecast_config), _P(C.c_int32), C.c_int32,
                                      C.c_int32, _P(C.c_int32), _P(C.c_double), _P(C.c_int32)]),
     "lp_eval_l1": (C.c_double, [_P(C.c_int32), _P(C.c_int32), C.c_int32]),
+    "lp_policy_defaults": (lp_policy, [C.c_int32]),
+    "lp_simulate": (C.c_int, [C.c_void_p, _P(lp_profile), _P(lp_costs), _P(lp_options), C.c_int32, _P(C.c_int32),
+                              C.c_int32, C.c_double, C.c_int32, _P(lp_policy), C.c_uint64, C.c_int32, C.c_double,
+                              C.c_double, _P(lp_sim_report), _P(lp_interval_log)]),
     "lp_max_instances": (C.c_int32, []),
     "lp_build_info": (C.c_char_p, []),
 }

@@ -375,3 +375,54 @@ def eval_l1(pred: Sequence[int], actual: Sequence[int]) -> float:
     a = (C.c_int32 * max(n, 1))(*pred)
     b = (C.c_int32 * max(n, 1))(*actual)
     return _abi.lib().lp_eval_l1(a, b, n)
+
+
+# ---- the replay driver: the reference simulator's run() ----
+POLICIES = {"proactive": _abi.LP_POLICY_PROACTIVE, "ideal": _abi.LP_POLICY_IDEAL,
+            "reactive": _abi.LP_POLICY_REACTIVE, "checkpoint": _abi.LP_POLICY_CHECKPOINT,
+            "redundancy": _abi.LP_POLICY_REDUNDANCY}
+_MIG_NAMES = ["none", "intra_stage", "inter_stage", "pipeline"]
+
+
+def policy(name: str, **kw) -> _abi.lp_policy:
+    """Policy (simulator.hpp:38-75) with the reference's defaults; keyword
+    arguments override lp_policy fields (lookahead, method, history,
+    ckpt_period_intervals, ckpt_save_cost_s, ..., redundancy_fixed_stages)."""
+    if name not in POLICIES:
+        raise ValueError(f"unknown policy: {name}")
+    p = _abi.lib().lp_policy_defaults(POLICIES[name])
+    for k, v in kw.items():
+        setattr(p, k, _method(v) if k == "method" else v)
+    return p
+
+
+def simulate(counts: Sequence[int], w: WorkloadProfile, pol: _abi.lp_policy, seed: int,
+             opt: Optional[PlannerOptions] = None, costs: Optional[CostTable] = None, interval_s: float = 60.0,
+             capacity: int = 0, epoch_samples: int = 0, spot_price_per_hour: float = 0.0,
+             ondemand_price_per_hour: float = 0.0, planner: Optional["Planner"] = None, device: int = 0):
+    """run(series, w, policy, seed, options, shared_planner) (simulator.cpp:119-340).
+    Returns (report dict, list of per-interval dicts) with the reference's
+    report_to_json field names."""
+    lib = _abi.lib()
+    p, keep = w.to_c()
+    c = (costs or CostTable()).to_c()
+    o = (opt or PlannerOptions()).to_c()
+    n = len(counts)
+    cnt = (C.c_int32 * max(n, 1))(*counts)
+    rep = _abi.lp_sim_report()
+    logs = (_abi.lp_interval_log * max(n, 1))()
+    _abi.check(lib.lp_simulate(planner._h if planner else None, C.byref(p), C.byref(c), C.byref(o), device, cnt, n,
+                               interval_s, capacity, C.byref(pol), seed, epoch_samples, spot_price_per_hour,
+                               ondemand_price_per_hour, C.byref(rep), logs))
+    led = lambda L: {"effective_s": L.effective_s, "migration_s": L.migration_s, "checkpoint_s": L.checkpoint_s,
+                     "wasted_rollback_s": L.wasted_rollback_s, "idle_s": L.idle_s}
+    report = {"seed": rep.seed, "committed_samples": rep.committed_samples, "wall_time_s": rep.wall_time_s,
+              "ledger": led(rep.ledger), "instance_seconds": rep.instance_seconds,
+              "instance_hours": rep.instance_hours, "spot_cost": rep.spot_cost, "ondemand_cost": rep.ondemand_cost,
+              "cost_per_sample": rep.cost_per_sample if rep.has_cost_per_sample else None,
+              "epochs_completed": rep.epochs_completed, "rollback_events": rep.rollback_events,
+              "suspended_intervals": rep.suspended_intervals, "sample_accounting_ok": bool(rep.sample_accounting_ok)}
+    ivs = [{"interval": L.interval, "available": L.available, "pipelines": L.pipelines, "stages": L.stages,
+            "throughput": L.throughput, "committed": L.committed, "rolled_back": L.rolled_back,
+            "migration": _MIG_NAMES[L.migration], "ledger": led(L.ledger)} for L in logs[:n]]
+    return report, ivs

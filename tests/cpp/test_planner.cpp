@@ -257,6 +257,22 @@ int main() {
     EXPECT(t.rollback && t.kind == MigrationKind::pipeline);
     EXPECT(resume_cost({3, 8}, w, costs) > t.cost_s);
   }
+  // ---- the replay driver (simulator.cpp:119-340)
+  {
+    IntervalSeries series;
+    series.capacity = 32;
+    series.counts = {32, 30, 30, 28, 31, 27, 27, 24, 26, 26, 22, 25, 25, 25, 20, 28, 32, 32, 29, 30};
+    SimOptions so;
+    so.planner.mc_trials = 1000;
+    for (Policy pol : {Policy::Reactive(), Policy::Checkpoint(), Policy::Ideal(), Policy::Proactive()}) {
+      SimReport r = run(series, lm_1p5b(), pol, 11, so);
+      EXPECT(r.intervals.size() == series.counts.size() && r.sample_accounting_ok);
+      double total = 0.0;
+      for (const IntervalLog& l : r.intervals) total += l.ledger.total();
+      EXPECT(std::abs(total - r.ledger.total()) < 1e-6 * (1.0 + total));
+      EXPECT(std::abs(r.ledger.total() - r.instance_seconds) < 1e-6 * r.instance_seconds);
+    }
+  }
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
