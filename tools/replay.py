@@ -105,9 +105,41 @@ def loop_proactive(plan_fn, reactive_fn, forecast_fn, depth_ok, counts, interval
     return seq, times
 
 
+def simulate_mode(a):
+    """The whole simulator run() (simulator.cpp:119-340) of config 3: the
+    ledger, rollbacks and sample accounting around 1440 re-plans, on this
+    library (lp_simulate) or the reference (oracle/_ref), seed 1."""
+    if a.mode == "sim-compare":
+        x = json.loads(Path(a.files[0]).read_text())
+        y = json.loads(Path(a.files[1]).read_text())
+        same = x["report"] == y["report"] and x["intervals"] == y["intervals"]
+        print(f"reports {'identical' if same else 'DIFFERENT'} ({len(x['intervals'])} intervals)")
+        sys.exit(0 if same else 1)
+    counts = json.loads(TRACE.read_text())["counts"][: a.intervals]
+    from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_6p7b
+    from paper_2403_14097_b200.planner import policy, simulate
+    w = lm_6p7b()
+    opt = PlannerOptions(mc_trials=a.trials)
+    pol = policy(a.policy)
+    t0 = time.perf_counter()
+    if a.mode == "sim-gpu":
+        rep, ivs = simulate(counts, w, pol, 1, opt, CostTable(), 60.0, 128)
+    else:
+        from oracle import oracle as O
+        rep, ivs = O.ref_simulate(counts, w, pol, 1, opt, CostTable(), 60.0, 128)
+    total = time.perf_counter() - t0
+    res = {"mode": a.mode, "policy": a.policy, "trials": a.trials, "intervals": len(ivs), "total_s": total,
+           "report": rep, "intervals": ivs}
+    print(json.dumps({k: v for k, v in res.items() if k not in ("report", "intervals")} |
+                     {"committed_samples": rep["committed_samples"], "rollback_events": rep["rollback_events"]}))
+    if a.out:
+        Path(a.out).parent.mkdir(parents=True, exist_ok=True)
+        Path(a.out).write_text(json.dumps(res))
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["trace", "gpu", "ref", "compare"])
+    ap.add_argument("mode", choices=["trace", "gpu", "ref", "compare", "sim-gpu", "sim-ref", "sim-compare"])
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--intervals", type=int, default=1440)
     ap.add_argument("--no-cache", action="store_true")
@@ -117,6 +149,8 @@ def main():
     a = ap.parse_args()
     if a.mode == "trace":
         return make_trace()
+    if a.mode.startswith("sim"):
+        return simulate_mode(a)
     if a.mode == "compare":
         x = json.loads(Path(a.files[0]).read_text())["sequence"]
         y = json.loads(Path(a.files[1]).read_text())["sequence"]
