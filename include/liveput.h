@@ -389,6 +389,17 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
                       uint64_t seed, int32_t epoch_samples, double spot_price_per_hour,
                       double ondemand_price_per_hour, lp_sim_report* report, lp_interval_log* logs);
 
+/* The same for many seeds at once: the configuration sequence (and so every
+ * re-plan) does not depend on the seed — only the placements and sample
+ * shuffles do — so the trace is planned once and each seed replays the
+ * bookkeeping.  reports: n_seeds; logs: n_seeds x len (seed-major). */
+lp_status lp_simulate_batch(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
+                            const lp_options* planner_options, int32_t device, const int32_t* counts,
+                            int32_t len, double interval_s, int32_t capacity, const lp_policy* policy,
+                            const uint64_t* seeds, int32_t n_seeds, int32_t epoch_samples,
+                            double spot_price_per_hour, double ondemand_price_per_hour,
+                            lp_sim_report* reports, lp_interval_log* logs);
+
 /* Build information (sm arch, sizes supported). */
 int32_t lp_max_instances(void);
 const char* lp_build_info(void);

@@ -204,6 +204,10 @@ _SIGS = {
     "lp_simulate": (C.c_int, [C.c_void_p, _P(lp_profile), _P(lp_costs), _P(lp_options), C.c_int32, _P(C.c_int32),
                               C.c_int32, C.c_double, C.c_int32, _P(lp_policy), C.c_uint64, C.c_int32, C.c_double,
                               C.c_double, _P(lp_sim_report), _P(lp_interval_log)]),
+    "lp_simulate_batch": (C.c_int, [C.c_void_p, _P(lp_profile), _P(lp_costs), _P(lp_options), C.c_int32,
+                                    _P(C.c_int32), C.c_int32, C.c_double, C.c_int32, _P(lp_policy), _P(C.c_uint64),
+                                    C.c_int32, C.c_int32, C.c_double, C.c_double, _P(lp_sim_report),
+                                    _P(lp_interval_log)]),
     "lp_max_instances": (C.c_int32, []),
     "lp_build_info": (C.c_char_p, []),
 }

@@ -140,47 +140,36 @@ Config reactive(int n, lp::Model& m) {
   return lp_config{c.d, c.p};
 }
 
-}  // namespace
-
-extern "C" {
-
-lp_policy lp_policy_defaults(int32_t kind) {
-  lp_policy p{};
-  p.kind = kind;
-  p.lookahead = 12;
-  p.method = LP_PREDICT_ARIMA;
-  p.history = 12;
-  p.ckpt_period_intervals = 5;
-  p.ckpt_save_cost_s = 10.0;
-  p.ckpt_restore_cost_s = 30.0;
-  p.ckpt_restart_cost_s = 30.0;
-  p.redundancy_fixed_stages = 4;
-  p.redundancy_slowdown = 0.75;
-  return p;
-}
-
-lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
-                      const lp_options* planner_options, int32_t device, const int32_t* counts,
-                      int32_t len, double interval_s, int32_t capacity, const lp_policy* policy,
-                      uint64_t seed, int32_t epoch_samples, double spot_price_per_hour,
-                      double ondemand_price_per_hour, lp_sim_report* report, lp_interval_log* logs) {
-  if (!profile || !costs || !planner_options || !policy || !report || !logs || (!counts && len > 0))
-    return sim_fail(LP_EINVAL, "simulate: null argument");
-  if (len <= 0) return sim_fail(LP_EINVAL, "run: empty series");
-  if (policy->kind < LP_POLICY_PROACTIVE || policy->kind > LP_POLICY_REDUNDANCY)
-    return sim_fail(LP_EINVAL, "simulate: unknown policy");
-  lp::Model model(*profile);
-  const double T = interval_s;
-  const int B = profile->minibatch_size;
-  const int epoch = epoch_samples > 0 ? epoch_samples : 64 * B;
+// Pass 1, seed-independent: the configuration of every interval.  Under the
+// planning policies it is adjust_config of the previous plan's first step
+// (simulator.cpp:196-199), and the plan only sees the trace and that
+// configuration — never the placements — so one planning pass serves every
+// seed of a batch.
+lp_status targets_of(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
+                     const lp_options* planner_options, int32_t device, const int32_t* counts, int32_t len,
+                     double T, int32_t capacity, const lp_policy* policy, lp::Model& model,
+                     std::vector<Config>& targets) {
   const int kind = policy->kind;
   const bool needs_plan = kind == LP_POLICY_PROACTIVE || kind == LP_POLICY_IDEAL;
-
+  targets.assign(len, std::nullopt);
+  if (!needs_plan) {
+    for (int i = 0; i < len; ++i) {
+      const int n = counts[i];
+      if (kind == LP_POLICY_REDUNDANCY) {
+        const int fs = policy->redundancy_fixed_stages;
+        const int d = fs > 0 ? n / fs : 0;
+        if (d >= 1 && model.depth_ok(fs)) targets[i] = lp_config{d, fs};
+      } else {
+        targets[i] = reactive(n, model);
+      }
+    }
+    return LP_OK;
+  }
   // the planner: the injected handle, or a private one with this run's T and
   // rollback penalty (simulator.cpp:126-130)
   lp_handle* h = shared;
   lp_handle* own = nullptr;
-  if (needs_plan && !h) {
+  if (!h) {
     lp_options o = *planner_options;
     o.interval_s = T;
     o.rollback_penalty_s = policy->ckpt_restore_cost_s;
@@ -195,7 +184,6 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
       if (h) lp_destroy(h);
     }
   } guard{own};
-
   // Proactive forecasts of every interval in one launch: window i of
   // [c0]*(H-1) + counts + I pad values is the history at interval i, padded
   // as simulator.cpp:311-313 does.
@@ -217,7 +205,36 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
     if (s != LP_OK) return s;
     if (nw < len) return sim_fail(LP_ECUDA, "simulate: forecast windows %d < %d", nw, len);
   }
+  Config planned;
+  std::vector<int32_t> ns;
+  std::vector<lp_plan_step> steps;
+  for (int i = 0; i < len; ++i) {
+    const int n = counts[i];
+    const Config target = (i == 0) ? reactive(n, model) : adjust(planned, n, model);
+    targets[i] = target;
+    ns.assign(1, n);
+    if (kind == LP_POLICY_IDEAL) {
+      for (int j = 1; j <= I; ++j) ns.push_back(i + j < len ? counts[i + j] : counts[len - 1]);
+    } else {
+      ns.insert(ns.end(), fc_all.begin() + static_cast<size_t>(i) * I, fc_all.begin() + static_cast<size_t>(i + 1) * I);
+    }
+    steps.resize(ns.size() - 1);
+    const lp_config cur = target ? *target : lp_config{0, 0};
+    lp_status s = lp_replan(h, cur, ns.data(), (int32_t)ns.size(), steps.data(), nullptr, 0, nullptr);
+    if (s != LP_OK) return sim_fail(s, "simulate: re-plan at interval %d: %s", i, lp_last_error(h));
+    planned = steps[0].config.pipelines > 0 ? Config(steps[0].config) : std::nullopt;
+  }
+  return LP_OK;
+}
 
+// Pass 2, per seed: placements, rollbacks, migration costs, commits and the
+// ledger (simulator.cpp:152-340) for the given configuration sequence.
+void run_seed(const std::vector<Config>& targets, const lp_profile* profile, const lp_costs* costs,
+              const int32_t* counts, int32_t len, double T, const lp_policy* policy, uint64_t seed, int epoch,
+              double spot_price_per_hour, double ondemand_price_per_hour, lp::Model& model,
+              lp_sim_report* report, lp_interval_log* logs) {
+  const int B = profile->minibatch_size;
+  const int kind = policy->kind;
   lp_sim_report rep{};
   rep.seed = seed;
   rep.sample_accounting_ok = 1;
@@ -227,11 +244,8 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
     double seconds = 0.0;
   };
   std::vector<Commit> commits(len);
-  Config cfg, planned;
+  Config cfg;
   int alive = 0, last_save = 0;
-  std::vector<int32_t> ns;
-  std::vector<lp_plan_step> steps;
-
   auto revoke = [&](int j) {
     Commit& c = commits[j];
     if (c.samples.empty()) return;
@@ -245,7 +259,6 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
     c.samples.clear();
     c.seconds = 0.0;
   };
-
   for (int i = 0; i < len; ++i) {
     const int n = counts[i];
     const int k_dead = std::max(0, alive - n);
@@ -264,21 +277,7 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
       for (int s : surv) wiped |= s == 0;
     }
 
-    Config target;
-    switch (kind) {
-      case LP_POLICY_REACTIVE:
-      case LP_POLICY_CHECKPOINT:
-        target = reactive(n, model);
-        break;
-      case LP_POLICY_REDUNDANCY: {
-        const int fs = policy->redundancy_fixed_stages;
-        const int d = fs > 0 ? n / fs : 0;
-        if (d >= 1 && model.depth_ok(fs)) target = lp_config{d, fs};
-        break;
-      }
-      default:
-        target = (i == 0) ? reactive(n, model) : adjust(planned, n, model);
-    }
+    const Config target = targets[i];
 
     lp_interval_log log{};
     log.interval = i;
@@ -310,8 +309,7 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
         int mn = cfg->pipelines;  // transition_outcome (migration.cpp:91-98)
         for (int s : surv) mn = std::min(mn, s);
         int32_t rb = 0;
-        lp_status s = lp_transition_outcome(profile, costs, mn, *cfg, *target, fresh, &mig_due, &mig_kind, &rb);
-        if (s != LP_OK) return s;
+        lp_transition_outcome(profile, costs, mn, *cfg, *target, fresh, &mig_due, &mig_kind, &rb);  // args valid
       }
     }
 
@@ -362,20 +360,6 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
     cfg = target;
     alive = n;
 
-    if (needs_plan) {
-      ns.assign(1, n);
-      if (kind == LP_POLICY_IDEAL) {
-        for (int j = 1; j <= I; ++j) ns.push_back(i + j < len ? counts[i + j] : counts[len - 1]);
-      } else {
-        ns.insert(ns.end(), fc_all.begin() + static_cast<size_t>(i) * I,
-                  fc_all.begin() + static_cast<size_t>(i + 1) * I);
-      }
-      steps.resize(ns.size() - 1);
-      const lp_config cur = cfg ? *cfg : lp_config{0, 0};
-      lp_status s = lp_replan(h, cur, ns.data(), (int32_t)ns.size(), steps.data(), nullptr, 0, nullptr);
-      if (s != LP_OK) return sim_fail(s, "simulate: re-plan at interval %d: %s", i, lp_last_error(h));
-      planned = steps[0].config.pipelines > 0 ? Config(steps[0].config) : std::nullopt;
-    }
   }
 
   for (int i = 0; i < len; ++i) {  // totals (simulator.cpp:321-329)
@@ -398,8 +382,61 @@ lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_cos
     rep.cost_per_sample = rep.spot_cost / static_cast<double>(rep.committed_samples);
   }
   rep.epochs_completed = samples.epochs();
+  (void)model;
   *report = rep;
+}
+
+}  // namespace
+
+extern "C" {
+
+lp_policy lp_policy_defaults(int32_t kind) {
+  lp_policy p{};
+  p.kind = kind;
+  p.lookahead = 12;
+  p.method = LP_PREDICT_ARIMA;
+  p.history = 12;
+  p.ckpt_period_intervals = 5;
+  p.ckpt_save_cost_s = 10.0;
+  p.ckpt_restore_cost_s = 30.0;
+  p.ckpt_restart_cost_s = 30.0;
+  p.redundancy_fixed_stages = 4;
+  p.redundancy_slowdown = 0.75;
+  return p;
+}
+
+lp_status lp_simulate_batch(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
+                            const lp_options* planner_options, int32_t device, const int32_t* counts,
+                            int32_t len, double interval_s, int32_t capacity, const lp_policy* policy,
+                            const uint64_t* seeds, int32_t n_seeds, int32_t epoch_samples,
+                            double spot_price_per_hour, double ondemand_price_per_hour,
+                            lp_sim_report* reports, lp_interval_log* logs) {
+  if (!profile || !costs || !planner_options || !policy || !reports || !logs || !seeds || n_seeds < 1 ||
+      (!counts && len > 0))
+    return sim_fail(LP_EINVAL, "simulate: null argument");
+  if (len <= 0) return sim_fail(LP_EINVAL, "run: empty series");
+  if (policy->kind < LP_POLICY_PROACTIVE || policy->kind > LP_POLICY_REDUNDANCY)
+    return sim_fail(LP_EINVAL, "simulate: unknown policy");
+  lp::Model model(*profile);
+  std::vector<Config> targets;
+  lp_status s = targets_of(shared, profile, costs, planner_options, device, counts, len, interval_s, capacity,
+                           policy, model, targets);
+  if (s != LP_OK) return s;
+  const int epoch = epoch_samples > 0 ? epoch_samples : 64 * profile->minibatch_size;
+  for (int q = 0; q < n_seeds; ++q)
+    run_seed(targets, profile, costs, counts, len, interval_s, policy, seeds[q], epoch, spot_price_per_hour,
+             ondemand_price_per_hour, model, reports + q, logs + static_cast<size_t>(q) * len);
   return LP_OK;
+}
+
+lp_status lp_simulate(lp_handle* shared, const lp_profile* profile, const lp_costs* costs,
+                      const lp_options* planner_options, int32_t device, const int32_t* counts,
+                      int32_t len, double interval_s, int32_t capacity, const lp_policy* policy,
+                      uint64_t seed, int32_t epoch_samples, double spot_price_per_hour,
+                      double ondemand_price_per_hour, lp_sim_report* report, lp_interval_log* logs) {
+  return lp_simulate_batch(shared, profile, costs, planner_options, device, counts, len, interval_s, capacity,
+                           policy, &seed, 1, epoch_samples, spot_price_per_hour, ondemand_price_per_hour,
+                           report, logs);
 }
 
 }  // extern "C"

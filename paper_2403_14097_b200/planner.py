@@ -396,6 +396,41 @@ def policy(name: str, **kw) -> _abi.lp_policy:
     return p
 
 
+def _report_dicts(rep, logs, n):
+    led = lambda L: {"effective_s": L.effective_s, "migration_s": L.migration_s, "checkpoint_s": L.checkpoint_s,
+                     "wasted_rollback_s": L.wasted_rollback_s, "idle_s": L.idle_s}
+    report = {"seed": rep.seed, "committed_samples": rep.committed_samples, "wall_time_s": rep.wall_time_s,
+              "ledger": led(rep.ledger), "instance_seconds": rep.instance_seconds,
+              "instance_hours": rep.instance_hours, "spot_cost": rep.spot_cost, "ondemand_cost": rep.ondemand_cost,
+              "cost_per_sample": rep.cost_per_sample if rep.has_cost_per_sample else None,
+              "epochs_completed": rep.epochs_completed, "rollback_events": rep.rollback_events,
+              "suspended_intervals": rep.suspended_intervals, "sample_accounting_ok": bool(rep.sample_accounting_ok)}
+    ivs = [{"interval": L.interval, "available": L.available, "pipelines": L.pipelines, "stages": L.stages,
+            "throughput": L.throughput, "committed": L.committed, "rolled_back": L.rolled_back,
+            "migration": _MIG_NAMES[L.migration], "ledger": led(L.ledger)} for L in logs[:n]]
+    return report, ivs
+
+
+def simulate_batch(counts: Sequence[int], w: WorkloadProfile, pol: _abi.lp_policy, seeds: Sequence[int],
+                   opt: Optional[PlannerOptions] = None, costs: Optional[CostTable] = None, interval_s: float = 60.0,
+                   capacity: int = 0, epoch_samples: int = 0, spot_price_per_hour: float = 0.0,
+                   ondemand_price_per_hour: float = 0.0, planner: Optional["Planner"] = None, device: int = 0):
+    """run() for every seed, planning the trace once (lp_simulate_batch)."""
+    lib = _abi.lib()
+    p, keep = w.to_c()
+    c = (costs or CostTable()).to_c()
+    o = (opt or PlannerOptions()).to_c()
+    n, m = len(counts), len(seeds)
+    cnt = (C.c_int32 * max(n, 1))(*counts)
+    sd = (C.c_uint64 * max(m, 1))(*seeds)
+    reps = (_abi.lp_sim_report * max(m, 1))()
+    logs = (_abi.lp_interval_log * max(n * m, 1))()
+    _abi.check(lib.lp_simulate_batch(planner._h if planner else None, C.byref(p), C.byref(c), C.byref(o), device,
+                                     cnt, n, interval_s, capacity, C.byref(pol), sd, m, epoch_samples,
+                                     spot_price_per_hour, ondemand_price_per_hour, reps, logs))
+    return [_report_dicts(reps[q], logs[q * n:(q + 1) * n], n) for q in range(m)]
+
+
 def simulate(counts: Sequence[int], w: WorkloadProfile, pol: _abi.lp_policy, seed: int,
              opt: Optional[PlannerOptions] = None, costs: Optional[CostTable] = None, interval_s: float = 60.0,
              capacity: int = 0, epoch_samples: int = 0, spot_price_per_hour: float = 0.0,
@@ -414,15 +449,4 @@ def simulate(counts: Sequence[int], w: WorkloadProfile, pol: _abi.lp_policy, see
     _abi.check(lib.lp_simulate(planner._h if planner else None, C.byref(p), C.byref(c), C.byref(o), device, cnt, n,
                                interval_s, capacity, C.byref(pol), seed, epoch_samples, spot_price_per_hour,
                                ondemand_price_per_hour, C.byref(rep), logs))
-    led = lambda L: {"effective_s": L.effective_s, "migration_s": L.migration_s, "checkpoint_s": L.checkpoint_s,
-                     "wasted_rollback_s": L.wasted_rollback_s, "idle_s": L.idle_s}
-    report = {"seed": rep.seed, "committed_samples": rep.committed_samples, "wall_time_s": rep.wall_time_s,
-              "ledger": led(rep.ledger), "instance_seconds": rep.instance_seconds,
-              "instance_hours": rep.instance_hours, "spot_cost": rep.spot_cost, "ondemand_cost": rep.ondemand_cost,
-              "cost_per_sample": rep.cost_per_sample if rep.has_cost_per_sample else None,
-              "epochs_completed": rep.epochs_completed, "rollback_events": rep.rollback_events,
-              "suspended_intervals": rep.suspended_intervals, "sample_accounting_ok": bool(rep.sample_accounting_ok)}
-    ivs = [{"interval": L.interval, "available": L.available, "pipelines": L.pipelines, "stages": L.stages,
-            "throughput": L.throughput, "committed": L.committed, "rolled_back": L.rolled_back,
-            "migration": _MIG_NAMES[L.migration], "ledger": led(L.ledger)} for L in logs[:n]]
-    return report, ivs
+    return _report_dicts(rep, logs, n)

@@ -8,7 +8,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_1p5b, lm_6p7b
-from paper_2403_14097_b200.planner import policy, simulate
+from paper_2403_14097_b200.planner import policy, simulate, simulate_batch
 
 needs_ref = pytest.mark.skipif(not O.ref_available(), reason="reference library not available")
 
@@ -51,3 +51,16 @@ def test_planning_policies_match_reference():
             rep, ivs = _check(w, name, cap, tr, 3, opt, CostTable())
             assert len(ivs) == len(tr)
     rep, _ = _check(lm_6p7b(), "proactive", 128, _traces()[2][1], 5, opt, CostTable(), method="moving_avg")
+
+
+@pytest.mark.gpu
+def test_batch_equals_single_runs():
+    """One planning pass for many seeds gives each seed's own run()."""
+    opt = PlannerOptions(mc_trials=2000)
+    cap, tr = _traces()[1]
+    for name in ("proactive", "checkpoint"):
+        pol = policy(name)
+        seeds = [1, 2, 3, 99]
+        batch = simulate_batch(tr, lm_1p5b(), pol, seeds, opt, CostTable(), capacity=cap)
+        for s, got in zip(seeds, batch):
+            assert got == simulate(tr, lm_1p5b(), pol, s, opt, CostTable(), capacity=cap)
