@@ -122,6 +122,13 @@ def simulate_mode(a):
     opt = PlannerOptions(mc_trials=a.trials)
     pol = policy(a.policy)
     t0 = time.perf_counter()
+    if a.mode == "sim-gpu" and a.seeds > 1:
+        from paper_2403_14097_b200.planner import simulate_batch
+        runs = simulate_batch(counts, w, pol, list(range(1, a.seeds + 1)), opt, CostTable(), 60.0, 128)
+        total = time.perf_counter() - t0
+        print(json.dumps({"mode": a.mode, "policy": a.policy, "trials": a.trials, "seeds": a.seeds, "total_s": total,
+                          "committed_samples": [r[0]["committed_samples"] for r in runs]}))
+        return
     if a.mode == "sim-gpu":
         rep, ivs = simulate(counts, w, pol, 1, opt, CostTable(), 60.0, 128)
     else:
@@ -143,7 +150,8 @@ def main():
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--intervals", type=int, default=1440)
     ap.add_argument("--no-cache", action="store_true")
-    ap.add_argument("--policy", choices=["ideal", "proactive"], default="ideal")
+    ap.add_argument("--policy", choices=["ideal", "proactive", "reactive", "checkpoint", "redundancy"], default="ideal")
+    ap.add_argument("--seeds", type=int, default=1, help="sim-gpu: seeds 1..S in one lp_simulate_batch")
     ap.add_argument("--out", default=None)
     ap.add_argument("files", nargs="*")
     a = ap.parse_args()
