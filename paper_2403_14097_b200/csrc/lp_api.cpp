@@ -787,6 +787,10 @@ struct lp_handle {
   std::vector<NodeCfg> cfg;
   std::vector<double4> pcost;  // per depth: pipe transfer, inter unit, resume cost
   std::vector<int4> lrows;
+  // per availability n: the level's nodes (configs of n + suspension) and
+  // the largest D per depth (n / P), built once — the profile is fixed
+  std::vector<std::vector<NodeCfg>> level_nodes;
+  std::vector<DenseMap<int>> level_depths;
   ThrTable thr;
   DpScalars S{};
   size_t off_divtab = 0;
@@ -1194,10 +1198,26 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   lbase[0] = 0;
   lcount[0] = 1;
   h->cfg.push_back({cur_on ? current.pipelines : 0, cur_on ? current.stages : 0, -1, 0});
+  auto nodes_of = [&](int n) -> const std::vector<NodeCfg>& {
+    if ((int)h->level_nodes.size() <= n) {
+      h->level_nodes.resize(n + 1);
+      h->level_depths.resize(n + 1);
+    }
+    std::vector<NodeCfg>& v = h->level_nodes[n];
+    if (v.empty()) {
+      for (const Cfg& c : h->model.configs(n)) {
+        v.push_back({c.d, c.p, -1, 0});
+        int& dm = h->level_depths[n][c.p];  // ascending P, the first D of a P is n / P
+        dm = std::max(dm, c.d);
+      }
+      v.push_back({0, 0, -1, 0});  // suspension is always reachable
+    }
+    return v;
+  };
   for (int j = 1; j <= H; ++j) {
     lbase[j] = (int)h->cfg.size();
-    for (const Cfg& c : h->model.configs(n_seq[j])) h->cfg.push_back({c.d, c.p, -1, 0});
-    h->cfg.push_back({0, 0, -1, 0});  // suspension is always reachable
+    const std::vector<NodeCfg>& v = nodes_of(n_seq[j]);
+    h->cfg.insert(h->cfg.end(), v.begin(), v.end());
     lcount[j] = (int)h->cfg.size() - lbase[j];
   }
   mark("levels");
@@ -1234,13 +1254,16 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
       spec_cur[si] = {current.pipelines, current.stages};
     } else if (!spec_full[si]) {
       spec_full[si] = 1;
-      int last_p = -1;
-      for (const Cfg& c : h->model.configs(n_now))  // ascending P, first D of a P = n/P
-        if (c.p != last_p) {
-          int& dm = sp.dmax_by_p[c.p];
-          dm = std::max(dm, c.d);
-          last_p = c.p;
+      nodes_of(n_now);
+      const DenseMap<int>& full = h->level_depths[n_now];
+      if (sp.dmax_by_p.size() == 0) {
+        sp.dmax_by_p = full;
+      } else {
+        for (const auto& [P, D] : full) {
+          int& dm = sp.dmax_by_p[P];
+          dm = std::max(dm, D);
         }
+      }
     }
     level_spec[j] = si;
   }
