@@ -273,6 +273,13 @@ uint64_t alg_ops(uint64_t scen, int k, int depths) {
 
 lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int nranks,
                           HistPlan& hp, std::string& err, int num_sms = 148) {
+  static const bool trace = getenv("LIVEPUT_TRACE_PREPARE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "[histplan] %-10s %8.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   hp = HistPlan();
   for (const EnsembleSpec& sp : specs) {
     const int n = sp.n, k = sp.k;
@@ -355,6 +362,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     hp.alg_ops += alg_ops(local, k, pd.n_entries);
   }
 
+  mark("pairs");
   // scenarios per block: enough blocks for ~24 per SM over all ensembles
   // (short blocks keep the last wave short; trial-sharded ranks keep every SM
   // busy), at most 8 per thread (measured: 2048 beats 4096 by 2% at N = 256)
@@ -365,7 +373,15 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   if (const char* pb = getenv("LIVEPUT_PER_BLOCK")) per_block = std::max<uint64_t>(256, strtoull(pb, nullptr, 10));
 
   // work items, grouped by launch configuration
-  std::map<std::tuple<int, int, int, int, int>, std::vector<std::pair<WorkItem, std::pair<size_t, int>>>> groups;
+  // one record per (pair, entry range): its work items are the chunks of
+  // the pair's trial range, expanded straight into hp.work below
+  struct Range {
+    WorkItem w;  // t0 / t1 set per chunk
+    uint64_t t_lo, t_hi, chunk;
+    size_t smem;
+    int aux;
+  };
+  std::map<std::tuple<int, int, int, int, int>, std::vector<Range>> groups;
   const char* kenv = getenv("LIVEPUT_HIST_KERNEL");
   const bool legacy = kenv && std::string(kenv) == "legacy";
   const bool inc_off = kenv && std::string(kenv) == "noinc";
@@ -401,8 +417,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         auto& gv1 = groups[{specs[pi].stage, 4, kreg * 16 + wmax, T, sm ? 1 : 0}];
-        gv1.reserve(gv1.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
-        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+        {
           WorkItem w{};
           w.pair = pi;
           w.e_lo = e;
@@ -411,9 +426,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_lo = hp.entries[e].evt_off;
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
-          w.t0 = t0;
-          w.t1 = std::min(pd.t_hi, t0 + chunk);
-          gv1.push_back({w, {smem, 0}});
+          gv1.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, 0});
         }
         e = e2;
       }
@@ -445,8 +458,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const size_t smem = smem_inc(e_res - e, km, pd.n, ev, sm, dlen, T);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         auto& gv2 = groups[{specs[pi].stage, 3, km, T, sm ? 1 : 0}];
-        gv2.reserve(gv2.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
-        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+        {
           WorkItem w{};
           w.pair = pi;
           w.e_lo = e;
@@ -457,9 +469,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.smem_evt = sm ? 1 : 0;
           w.dtab_off = doff;
           w.dtab_len = dlen;
-          w.t0 = t0;
-          w.t1 = std::min(pd.t_hi, t0 + chunk);
-          gv2.push_back({w, {smem, 0}});
+          gv2.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, 0});
         }
         e = e2;
       }
@@ -494,8 +504,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         auto& gv3 = groups[{specs[pi].stage, 2, kreg, T, sm ? 1 : 0}];
-        gv3.reserve(gv3.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
-        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+        {
           WorkItem w{};
           w.pair = pi;
           w.e_lo = e;
@@ -504,9 +513,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_lo = hp.entries[e].evt_off;
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
-          w.t0 = t0;
-          w.t1 = std::min(pd.t_hi, t0 + chunk);
-          gv3.push_back({w, {smem, uw}});
+          gv3.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, uw});
         }
         e = e2;
       }
@@ -530,7 +537,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
         const bool sm = smem_regs(e2 - e, km, pd.n, ev, true) <= kSmemBudgetR;
         const size_t smem = smem_regs(e2 - e, km, pd.n, ev, sm);
-        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += kChunkR) {
+        {
           WorkItem w{};
           w.pair = pi;
           w.e_lo = e;
@@ -539,9 +546,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
           w.e_res_hi = e_res;
-          w.t0 = t0;
-          w.t1 = std::min(pd.t_hi, t0 + kChunkR);
-          groups[{specs[pi].stage, 0, km, 256, sm ? 1 : 0}].push_back({w, {smem, 0}});
+          groups[{specs[pi].stage, 0, km, 256, sm ? 1 : 0}].push_back({w, pd.t_lo, pd.t_hi, (uint64_t)kChunkR, smem, 0});
         }
         e = e2;
       }
@@ -567,8 +572,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const size_t smem = smem_ctr(e2 - e, pd.k, pd.n, ev, sm, T, pmax);
         const uint64_t chunk = (uint64_t)T * 8;
         auto& gv4 = groups[{specs[pi].stage, 1, 0, T, sm ? 1 : 0}];
-        gv4.reserve(gv4.size() + (pd.t_hi - pd.t_lo + chunk - 1) / chunk);
-        for (uint64_t t0 = pd.t_lo; t0 < pd.t_hi; t0 += chunk) {
+        {
           WorkItem w{};
           w.pair = pi;
           w.e_lo = e;
@@ -576,13 +580,18 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_lo = hp.entries[e].evt_off;
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
-          w.t0 = t0;
-          w.t1 = std::min(pd.t_hi, t0 + chunk);
-          gv4.push_back({w, {smem, pmax}});
+          gv4.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, pmax});
         }
         e = e2;
       }
     }
+  }
+  mark("items");
+  {
+    size_t total = 0;
+    for (const auto& [key, items] : groups)
+      for (const Range& r : items) total += (r.t_hi - r.t_lo + r.chunk - 1) / r.chunk;
+    hp.work.reserve(total);
   }
   for (auto& [key, items] : groups) {
     Group g;
@@ -592,27 +601,26 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     g.threads = std::get<3>(key);
     g.smem_evt = std::get<4>(key) != 0;
     g.first = (int)hp.work.size();
-    g.count = (int)items.size();
-    for (auto& it : items) {
-      g.pmax_cap = std::max(g.pmax_cap, it.second.second);
-    }
-    for (auto& it : items) {
-      hp.work.push_back(it.first);
-      size_t s = it.second.first;
-      if (g.kind == 2) {
-        const PairDesc& pd = hp.pairs[it.first.pair];
-        s = smem_scn(it.first.e_res_hi - it.first.e_lo, pd.k, pd.n, it.first.evt_len, g.smem_evt,
-                     g.threads, g.pmax_cap);
+    for (const Range& r : items) g.pmax_cap = std::max(g.pmax_cap, r.aux);
+    for (const Range& r : items) {
+      size_t sm = r.smem;
+      const PairDesc& pd = hp.pairs[r.w.pair];
+      if (g.kind == 2)
+        sm = smem_scn(r.w.e_res_hi - r.w.e_lo, pd.k, pd.n, r.w.evt_len, g.smem_evt, g.threads, g.pmax_cap);
+      if (g.kind == 1)
+        sm = smem_ctr(r.w.e_hi - r.w.e_lo, pd.k, pd.n, r.w.evt_len, g.smem_evt, g.threads, g.pmax_cap);
+      g.smem = std::max(g.smem, sm);
+      for (uint64_t t0 = r.t_lo; t0 < r.t_hi; t0 += r.chunk) {
+        WorkItem w = r.w;
+        w.t0 = t0;
+        w.t1 = std::min(r.t_hi, t0 + r.chunk);
+        hp.work.push_back(w);
       }
-      if (g.kind == 1) {
-        const PairDesc& pd = hp.pairs[it.first.pair];
-        s = smem_ctr(it.first.e_hi - it.first.e_lo, pd.k, pd.n, it.first.evt_len, g.smem_evt,
-                     g.threads, g.pmax_cap);
-      }
-      g.smem = std::max(g.smem, s);
     }
+    g.count = (int)hp.work.size() - g.first;
     hp.groups.push_back(g);
   }
+  mark("groups");
   // stage ranges (specs come with non-decreasing stages)
   int nst = 0;
   for (const EnsembleSpec& sp : specs) nst = std::max(nst, sp.stage + 1);
