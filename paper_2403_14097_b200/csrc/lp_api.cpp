@@ -1385,22 +1385,24 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   // store slots of the fresh entries (appended; old slots of recomputed
   // ensembles are abandoned until the next eviction)
   h->store_off.assign(h->hp.entries.size(), 0);
-  for (size_t e = 0; e < h->hp.entries.size(); ++e) {
-    const EntryDesc& E = h->hp.entries[e];
-    const PairDesc& pd = h->hp.pairs[E.pair];
-    h->store_off[e] = (int32_t)h->store_used;
-    h->store_idx[{pd.n, pd.k}].ents[E.P] = {E.Dmax, (int)h->store_used};
-    h->store_used += hist_row(E.Dmax + 1, pd.k);
-  }
   for (const PairDesc& pd : h->hp.pairs) {
-    auto& slot = h->store_idx[{pd.n, pd.k}];
+    auto& slot = h->store_idx[{pd.n, pd.k}];  // one lookup per pair
     slot.count = pd.count;
-    std::vector<uint8_t> fresh_p(pd.n + 2, 0);  // drop stale depth slots
-    for (int e = pd.entry_base; e < pd.entry_base + pd.n_entries; ++e) fresh_p[h->hp.entries[e].P] = 1;
-    std::vector<int> stale;
-    for (const auto& [P, v] : slot.ents)
-      if (P >= (int)fresh_p.size() || !fresh_p[P]) stale.push_back(P);
-    for (int P : stale) slot.ents.erase(P);
+    const int e0 = pd.entry_base, e1 = pd.entry_base + pd.n_entries;
+    if (slot.ents.size() > 0) {  // a cached slot: drop the depths this plan does not refresh
+      std::vector<uint8_t> fresh_p(pd.n + 2, 0);
+      for (int e = e0; e < e1; ++e) fresh_p[h->hp.entries[e].P] = 1;
+      std::vector<int> stale;
+      for (const auto& [P, v] : slot.ents)
+        if (P >= (int)fresh_p.size() || !fresh_p[P]) stale.push_back(P);
+      for (int P : stale) slot.ents.erase(P);
+    }
+    for (int e = e0; e < e1; ++e) {
+      const EntryDesc& E = h->hp.entries[e];
+      h->store_off[e] = (int32_t)h->store_used;
+      slot.ents[E.P] = {E.Dmax, (int)h->store_used};
+      h->store_used += hist_row(E.Dmax + 1, pd.k);
+    }
   }
   {
     lp_status gs = grow_store(h, h->store_used);
