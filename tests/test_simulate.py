@@ -64,3 +64,16 @@ def test_batch_equals_single_runs():
         batch = simulate_batch(tr, lm_1p5b(), pol, seeds, opt, CostTable(), capacity=cap)
         for s, got in zip(seeds, batch):
             assert got == simulate(tr, lm_1p5b(), pol, s, opt, CostTable(), capacity=cap)
+
+
+def test_batch_non_planning_equals_single_runs():
+    """The batch entry point for the policies that never plan (CPU only)."""
+    opt = PlannerOptions(mc_trials=1000)
+    cap, tr = 64, [64, 60, 61, 55, 58, 50, 50, 47, 52, 49, 40, 44, 48, 48, 45, 30, 35, 44, 50, 52]
+    for name in ("reactive", "checkpoint"):
+        pol = policy(name)
+        seeds = [3, 4, 5]
+        batch = simulate_batch(tr, lm_1p5b(), pol, seeds, opt, CostTable(), capacity=cap)
+        for s, got in zip(seeds, batch):
+            assert got == simulate(tr, lm_1p5b(), pol, s, opt, CostTable(), capacity=cap)
+            assert got[0]["seed"] == s
