@@ -171,6 +171,30 @@ def test_table_generator_vs_oracle():
         p.close()
 
 
+def test_maximum_size_ensembles_vs_oracle():
+    """n = kMaxN = 2048 (the scenario-major kernel past n = 512), sparse and
+    dense preemption, and a re-plan at n = 1024 against the cache-free oracle."""
+    w = resnet152_dp()
+    assert O.oracle_configs(w, 2048)
+    for n, k in [(2048, 20), (2048, 200), (1500, 5)]:
+        trials = 2000
+        p = planner(w, PlannerOptions(mc_trials=trials, exact_cap=0))
+        cs = O.oracle_configs(w, n)
+        sel = cs[:: max(1, len(cs) // 12)]
+        ref, tot = O.oracle_ensemble_counts(n, k, False, trials, O.planner_seed(0x5EED, n, k), sel)
+        for ci, c in enumerate(sel):
+            got, gt = p.survivor_counts(c, n, k)
+            assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, c)
+        p.close()
+    ns = [1024, 1000, 1010]
+    opt = PlannerOptions(mc_trials=1000)
+    cur = O.oracle_reactive(w, ns[0])
+    ref = O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns)
+    p = planner(w, opt)
+    assert plan_rows(p.dp_optimize(cur, ns)) == plan_rows(ref)
+    p.close()
+
+
 # ---- phi, plans ---------------------------------------------------------------
 def test_phi_matches_reference():
     for c in load_golden("phi"):
