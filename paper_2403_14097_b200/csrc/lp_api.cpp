@@ -1344,6 +1344,20 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     const bool staged = want > 1 && fresh.size() >= 2 && scen >= (1u << 18);
     // shrinking stages: the DP left to run after the last one is short
     static const double kCuts[5][4] = {{1.0}, {0.75, 1.0}, {0.5, 0.85, 1.0}, {0.4, 0.7, 0.9, 1.0}, {}};
+    static const std::vector<double> env_cuts = [] {  // LIVEPUT_STAGE_CUTS=0.5,0.8,0.95 (A/B)
+      std::vector<double> c;
+      if (const char* e = getenv("LIVEPUT_STAGE_CUTS")) {
+        std::string v(e);
+        size_t pos = 0;
+        while (pos < v.size()) {
+          const size_t q = v.find(',', pos);
+          c.push_back(atof(v.substr(pos, q == std::string::npos ? std::string::npos : q - pos).c_str()));
+          if (q == std::string::npos) break;
+          pos = q + 1;
+        }
+      }
+      return c;
+    }();
     uint64_t cum = 0;
     int last = 0;
     for (size_t i = 0; i < fresh.size(); ++i) {
@@ -1353,7 +1367,11 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
           st = (int)std::min<size_t>(i, want - 1);
         } else {
           const double mid = (static_cast<double>(cum) + 0.5 * static_cast<double>(cost[i])) / static_cast<double>(total);
-          while (st < want - 1 && mid > kCuts[want - 1][st]) ++st;
+          if (!env_cuts.empty()) {
+            while (st < (int)env_cuts.size() && st < (int)lp_handle::kMaxStages - 1 && mid > env_cuts[st]) ++st;
+          } else {
+            while (st < want - 1 && mid > kCuts[want - 1][st]) ++st;
+          }
         }
       }
       st = std::max(st, last);
@@ -1375,6 +1393,14 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
       const int si = level_spec[j];
       if (si >= 0 && fresh_of[si] >= 0) need = std::max(need, fresh[fresh_of[si]].stage);
       h->level_need[j] = need;
+    }
+    if (trace) {
+      fprintf(stderr, "[prepare] stages:");
+      for (size_t i = 0; i < fresh.size(); ++i)
+        fprintf(stderr, " (%d,%d)s%d:%.0f%%", fresh[i].n, fresh[i].k, fresh[i].stage, 100.0 * cost[i] / std::max<uint64_t>(total, 1));
+      fprintf(stderr, "\n[prepare] level need:");
+      for (int j = 0; j < H; ++j) fprintf(stderr, " %d", h->level_need[j]);
+      fprintf(stderr, "\n");
     }
   }
   mark("specs");
