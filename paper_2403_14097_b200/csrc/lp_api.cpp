@@ -271,6 +271,24 @@ uint64_t alg_ops(uint64_t scen, int k, int depths) {
   return scen * (20ull + 35ull * k + 6ull * k * (uint64_t)depths);
 }
 
+// Rng::below(b) constants (rng.hpp:23-30) for b = 1 .. kMaxN, computed once
+// (two 64-bit divisions each).
+const DrawConst& draw_const(uint32_t b) {
+  static const std::vector<DrawConst> table = [] {
+    std::vector<DrawConst> t(kMaxN + 1);
+    for (uint32_t v = 1; v <= (uint32_t)kMaxN; ++v) {
+      DrawConst d{};
+      d.b = v;
+      d.lim = UINT64_MAX - UINT64_MAX % v;
+      d.fm = UINT64_MAX / v + 1;
+      d.c32 = (uint32_t)((1ull << 32) % v);
+      t[v] = d;
+    }
+    return t;
+  }();
+  return table[b];
+}
+
 lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int nranks,
                           HistPlan& hp, std::string& err, int num_sms = 148) {
   static const bool trace = getenv("LIVEPUT_TRACE_PREPARE") != nullptr;
@@ -307,7 +325,12 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       e.P = P;
       e.Dmax = Dm;
       e.lim = P * Dm;
-      e.magic = P >= 2 ? (uint32_t)((1ull << 32) / (uint64_t)P + 1ull) : 0u;
+      static const std::vector<uint32_t> magic = [] {  // floor(2^32 / P) + 1, P <= kMaxN
+        std::vector<uint32_t> m(kMaxN + 1, 0u);
+        for (int q = 2; q <= kMaxN; ++q) m[q] = (uint32_t)((1ull << 32) / (uint64_t)q + 1ull);
+        return m;
+      }();
+      e.magic = P >= 2 ? magic[P] : 0u;
       e.tmax = std::min(k, Dm);
       e.evt_off = (int)hp.evt_len;
       hp.evt_len += (int64_t)std::max(0, e.tmax - 1) * Dm;
@@ -344,14 +367,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       hp.exact_pairs++;
     } else {
       pd.draw_off = (int)hp.draws.size();
-      for (int i = 0; i < k; ++i) {
-        DrawConst d{};
-        d.b = (uint32_t)(n - i);
-        d.lim = UINT64_MAX - UINT64_MAX % d.b;
-        d.fm = UINT64_MAX / d.b + 1;
-        d.c32 = (uint32_t)((1ull << 32) % d.b);
-        hp.draws.push_back(d);
-      }
+      for (int i = 0; i < k; ++i) hp.draws.push_back(draw_const((uint32_t)(n - i)));
       hp.mc_pairs++;
     }
     hp.pairs.push_back(pd);
