@@ -2,6 +2,7 @@
 launch lists).  Cases:
   bench    BASELINE configs[3] (N=256, I=24, 1e6, k up to 40: counter variant)
   predict  N=256, I=12, 1e6, forecast-like drops k <= 8 (register variant)
+  n32      N=32, I=12, the known-answer sequence (latency floor; use --trials 10000)
 """
 import argparse
 import sys
@@ -12,12 +13,13 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 from bench import north_star_nseq  # noqa: E402
 
+N32 = [32, 28, 28, 26, 29, 26, 26, 21, 23, 23, 21, 25, 22]  # SURVEY §8c known-answer sequence
 PREDICT = [256, 250, 252, 245, 245, 248, 240, 236, 238, 232, 232, 229, 226]
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="bench", choices=["bench", "predict", "ns12"])
+    ap.add_argument("--case", default="bench", choices=["bench", "predict", "ns12", "n32"])
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
@@ -25,7 +27,7 @@ def main():
     from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_1p5b
     from paper_2403_14097_b200.planner import Planner, reactive_plan
     w = lm_1p5b()
-    ns = {"bench": north_star_nseq(256, 24), "predict": PREDICT, "ns12": north_star_nseq(256, 12)}[a.case]
+    ns = {"bench": north_star_nseq(256, 24), "predict": PREDICT, "ns12": north_star_nseq(256, 12), "n32": N32}[a.case]
     p = Planner(w, CostTable(), PlannerOptions(mc_trials=a.trials))
     cur = reactive_plan(ns[0], w)
     p.prepare(cur, ns)
