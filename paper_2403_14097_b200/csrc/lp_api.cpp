@@ -1722,13 +1722,19 @@ lp_status exec_dp(lp_handle* h) {
     LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
     LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
     int waited = -1;
+    static const bool pdl_on = [] {  // LIVEPUT_PDL=0: plain stream order between levels (A/B)
+      const char* e = getenv("LIVEPUT_PDL");
+      return !(e && e[0] == '0');
+    }();
     for (int j = 0; j < h->horizon; ++j) {
       const int need = j < (int)h->level_need.size() ? h->level_need[j] : nst - 1;
+      bool pdl = pdl_on && j > 0;  // right after a cross-stream wait: plain order
       if (need > waited) {
         LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[need], 0));
         waited = need;
+        pdl = false;
       }
-      LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, st, lv, cfg, pcost,
+      LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, pdl, st, lv, cfg, pcost,
                                 histp, thr, throw_, h->S, val, mig, par, stc, stm));
       ++launches;
     }

@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __
                                                       double* __restrict__ stc,
                                                       double* __restrict__ stm) {
   __shared__ Cand s_best[16];
+  // Programmatic dependent launch: level j+1 may start once every block of
+  // level j runs; its prologue (tables only) then overlaps this level, and
+  // griddepcontrol.wait below holds it until level j's values are visible.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const LevelDesc L = levels[j];
   if (static_cast<int>(blockIdx.x) >= L.next_count) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -338,6 +342,7 @@ __global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __
     nc.resume = pc.z;
   }
   const PhiConst K = phi_const(L, S, nc);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // level j-1's val / mig
   Cand best{0.0, 0.0, 0.0, 0.0, -1};
   // full take-order key (value desc, mig asc, index asc): prevs may be
   // folded out of index order below
@@ -515,7 +520,7 @@ __global__ void phi_single_kernel(NodeCfg pv, NodeCfg nx, NodeCost nc, LevelDesc
 }
 
 // ---------------------------------------------------------------------------
-cudaError_t launch_dp_step(int j, int next_count, int prev_count, cudaStream_t st,
+cudaError_t launch_dp_step(int j, int next_count, int prev_count, bool pdl, cudaStream_t st,
                            const LevelDesc* levels, const NodeCfg* cfg, const double4* pcost,
                            const double* histp, const double* thr_tab, const int32_t* thr_row,
                            const DpScalars& S, double* val, double* mig, int32_t* parent,
@@ -530,9 +535,17 @@ cudaError_t launch_dp_step(int j, int next_count, int prev_count, cudaStream_t s
     return (v >= 32 && v <= 512) ? v : 128;
   }();
   const int threads = std::min(cap, std::max(32, (prev_count + 31) / 32 * 32));
-  dp_step_kernel<<<blocks, threads, 0, st>>>(j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val,
-                                             mig, parent, stc, stm);
-  return cudaGetLastError();
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(blocks);
+  lc.blockDim = dim3(threads);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, dp_step_kernel, j, levels, cfg, pcost, histp, thr_tab, thr_row, S, val, mig,
+                            parent, stc, stm);
 }
 
 cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,

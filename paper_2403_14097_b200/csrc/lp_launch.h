@@ -38,7 +38,8 @@ cudaError_t launch_dump(int n, int k, int exact, int trials, uint64_t seed, cons
                         uint16_t* sorted_out, const int2* cfgs, int n_cfg, uint16_t* m_out,
                         cudaStream_t st);
 
-cudaError_t launch_dp_step(int j, int next_count, int prev_count, cudaStream_t st,
+// pdl: programmatic dependent launch on the previous level's kernel
+cudaError_t launch_dp_step(int j, int next_count, int prev_count, bool pdl, cudaStream_t st,
                            const LevelDesc* levels,
                            const NodeCfg* cfg, const double4* pcost, const double* histp,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
