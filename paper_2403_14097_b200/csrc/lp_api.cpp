@@ -825,6 +825,8 @@ struct lp_handle {
   int max_next = 0;         // largest level (next role), for the persistent DP grid
   bool live_pending = false;  // liveput rows of the last execute not yet computed
   bool dp_launches = false;  // LIVEPUT_DP=launches: one kernel per level (A/B)
+  bool dp_staged = true;     // LIVEPUT_DP_STAGED=0: never stage the DP in shared memory (A/B)
+  int dp_staged_nprob = -1;  // >= 0: this re-plan's persistent DP runs staged
   DevBuf tables, work;
   PinBuf pin_up, pin_down;
   size_t up_bytes = 0;
@@ -1092,6 +1094,8 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
   {
     const char* e = getenv("LIVEPUT_DP");
     h->dp_launches = (e && std::string(e) == "launches");
+    const char* es = getenv("LIVEPUT_DP_STAGED");
+    h->dp_staged = !(es && es[0] == '0');
   }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = h;
@@ -1588,6 +1592,18 @@ lp_status prepare_dp(lp_handle* h) {
   mark("lrows");
   h->max_next = 0;
   for (const LevelDesc& L : h->levels) h->max_next = std::max(h->max_next, L.next_count);
+  // shared-memory staged persistent DP (lp_dp.cu) when the whole DP input
+  // fits in a block's shared memory next to 3 more blocks per SM
+  h->dp_staged_nprob = -1;
+  if (h->dp_staged && H <= 64) {
+    long long nprob = 0;
+    for (int j = 0; j < H; ++j) {
+      const LevelDesc& L = h->levels[j];
+      if (L.has_hist) nprob += (long long)L.prev_count * (std::min(L.k, L.n_now) + 1);
+    }
+    const int n_nodes = h->levels[H - 1].next_base + h->levels[H - 1].next_count;
+    if (nprob < (1 << 20) && dp_staged_smem(n_nodes, H, (int)nprob) <= 40 * 1024) h->dp_staged_nprob = (int)nprob;
+  }
   size_t bytes = 0;
   lp_status us = upload_image(h,
                               {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
@@ -1709,6 +1725,7 @@ lp_status exec_dp(lp_handle* h) {
     a.final_value = dptr<double>(h->work, h->w_final);
     a.barrier = dptr<uint32_t>(h->work, h->w_bar);
     a.horizon = h->horizon;
+    a.max_next = std::max(1, h->max_next);
     static const bool trace = getenv("LIVEPUT_DP_TRACE") != nullptr;
     if (trace) {
       const size_t nb = (size_t)h->num_sms * 8 * (2 * kTraceLevels + 2);
@@ -1716,7 +1733,9 @@ lp_status exec_dp(lp_handle* h) {
       LP_CUDA(h, cudaMemsetAsync(h->dp_trace.p, 0, nb * 8, st));
       a.trace = static_cast<uint64_t*>(h->dp_trace.p);
     }
-    LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S));
+    const LevelDesc& last = h->levels[h->horizon - 1];
+    LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S,
+                                    last.next_base + last.next_count, h->dp_staged_nprob));
     ++launches;
   } else {
     LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
@@ -1818,6 +1837,10 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_
       for (int b = 0; b < used; ++b) {
         const uint64_t s0 = tr[(size_t)b * per + 3 + 2 * (j - 1)], c = tr[(size_t)b * per + 2 + 2 * j],
                        e = tr[(size_t)b * per + 3 + 2 * j];
+        if (s0 == 0 || e == 0) {  // left after the normalisation barrier
+          comp.push_back(0.0);
+          continue;
+        }
         smin = std::min(smin, s0);
         emax = std::max(emax, e);
         comp.push_back((double)(c - s0) * 1e-3);

@@ -596,28 +596,75 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   return v;
 }
 
-// Monotone arrival counter (zeroed before the launch): barrier e completes
-// when e * gridDim.x blocks have arrived.
-__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t& epoch) {
+// Monotone arrival counter (zeroed before the launch): a barrier completes
+// when the counter reaches `target`, the running total of the blocks taking
+// part in every barrier so far (all blocks for the first, the level blocks
+// after it).
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
   __syncthreads();
-  ++epoch;
   if (threadIdx.x == 0) {
-    const uint32_t target = epoch * gridDim.x;
     __threadfence();
     atomicAdd(ctr, 1u);
-    while (ld_relaxed_u32(ctr) < target) __nanosleep(100);
+    while (ld_relaxed_u32(ctr) < target) __nanosleep(32);
     __threadfence();  // acquire: orders the block's later reads after the arrivals
   }
   __syncthreads();
 }
 
 
-__global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScalars S) {
+// STAGED (small re-plans, N ~ 16..48): every block copies the node list, its
+// own next nodes' cost terms for every level, and all prev probability rows
+// into shared memory up front, with all the loads in flight at once.  A level
+// then reads only the previous level's values from L2; the dependent
+// level -> node -> cost -> row load chain (~2 us of a ~5 us level at N=32)
+// is gone.  Dynamic shared layout: cfg [n_nodes] | levels [H] | cost [H] |
+// row bases [H + 1] | probabilities; level j's prev rows sit at
+// base_j + i * (min(k_j, n_now_j) + 1).
+struct StagedLayout {
+  int n_nodes, horizon, n_prob;
+  __host__ __device__ size_t cfg_off() const { return 0; }
+  __host__ __device__ size_t lv_off() const { return (size_t)n_nodes * sizeof(NodeCfg); }
+  __host__ __device__ size_t nc_off() const { return lv_off() + (size_t)horizon * sizeof(LevelDesc); }
+  __host__ __device__ size_t base_off() const { return nc_off() + (size_t)horizon * sizeof(NodeCost); }
+  __host__ __device__ size_t prob_off() const {
+    return (base_off() + (size_t)(horizon + 1) * sizeof(int) + 15) & ~static_cast<size_t>(15);
+  }
+  __host__ __device__ size_t bytes() const { return prob_off() + (size_t)n_prob * sizeof(double); }
+};
+
+template <bool STAGED>
+__global__ void __launch_bounds__(256, STAGED ? 2 : 4) dp_persistent_kernel(DpArgs a, DpScalars S, StagedLayout G) {
   __shared__ Cand s_best[8];
   __shared__ int s_idx[256];
   __shared__ int s_path[kMaxHorizon + 1];
-  uint32_t epoch = 0;
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  NodeCfg* s_cfg = reinterpret_cast<NodeCfg*>(sm_raw + G.cfg_off());
+  LevelDesc* s_lv = reinterpret_cast<LevelDesc*>(sm_raw + G.lv_off());
+  NodeCost* s_nc = reinterpret_cast<NodeCost*>(sm_raw + G.nc_off());
+  int* s_base = reinterpret_cast<int*>(sm_raw + G.base_off());
+  double* s_prob = reinterpret_cast<double*>(sm_raw + G.prob_off());
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto next_cost = [&](const NodeCfg& nx) {
+    NodeCost nc{0.0, 0.0, 0.0, 0.0};
+    if (nx.d > 0) {
+      const double4 pc = a.pcost[nx.p];
+      nc.thr = a.thr_tab[a.thr_row[nx.p] + nx.d];
+      nc.pipe = pc.x;
+      nc.unit = pc.y;
+      nc.resume = pc.z;
+    }
+    return nc;
+  };
+  if (STAGED) {  // tables (independent of phase 0's output)
+    for (int i = threadIdx.x; i < G.n_nodes; i += blockDim.x) s_cfg[i] = a.cfg[i];
+    for (int j = threadIdx.x; j < G.horizon; j += blockDim.x) {
+      const LevelDesc L = a.levels[j];
+      s_lv[j] = L;
+      NodeCost nc{0.0, 0.0, 0.0, 0.0};
+      if (static_cast<int>(blockIdx.x) < L.next_count) nc = next_cost(a.cfg[L.next_base + blockIdx.x]);
+      s_nc[j] = nc;
+    }
+  }
   auto stamp = [&](int slot) {  // LIVEPUT_DP_TRACE: per-block globaltimer stamps
     if (a.trace && threadIdx.x == 0) {
       uint64_t t;
@@ -644,23 +691,47 @@ __global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScala
     a.mig[0] = 0.0;
   }
   stamp(1);
-  grid_barrier(a.barrier, epoch);
+  uint32_t target = gridDim.x;
+  grid_barrier(a.barrier, target);
+  // only the blocks that own a next node at some level take part from here;
+  // the others were there for the normalisation
+  const uint32_t active = min(gridDim.x, static_cast<uint32_t>(a.max_next));
+  if (blockIdx.x >= active) return;
+  if (STAGED) {  // every prev row the DP reads, from the store (now complete)
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int j = 0; j < G.horizon; ++j) {
+        s_base[j] = b;
+        const LevelDesc& L = s_lv[j];
+        if (L.has_hist) b += L.prev_count * (min(L.k, L.n_now) + 1);
+      }
+      s_base[G.horizon] = b;
+    }
+    __syncthreads();
+    const int n_prev = s_lv[G.horizon - 1].next_base;
+    for (int gi = threadIdx.x; gi < n_prev; gi += blockDim.x) {
+      int j = 0;
+      while (j + 1 < G.horizon && s_lv[j + 1].prev_base <= gi) ++j;
+      const LevelDesc& L = s_lv[j];
+      const NodeCfg pv = s_cfg[gi];
+      if (!L.has_hist || pv.d <= 0 || pv.hist_off < 0) continue;
+      const int stride = min(L.k, L.n_now) + 1, len = min(L.k, pv.d) + 1;
+      const double* src = a.store + pv.hist_off;
+      double* dst = s_prob + s_base[j] + (gi - L.prev_base) * stride;
+      for (int d = 0; d < len; ++d) dst[d] = src[d];
+    }
+    __syncthreads();
+  }
 
   // phases 1..H: F_{j+1}[c'] = max_c F_j[c] + phi(c, c'), one block per next node
   const double* histp = a.store;
   for (int j = 0; j < a.horizon; ++j) {
-    const LevelDesc L = a.levels[j];
+    const LevelDesc L = STAGED ? s_lv[j] : a.levels[j];
+    const int stride = min(L.k, L.n_now) + 1;
     for (int nb = blockIdx.x; nb < L.next_count; nb += gridDim.x) {
       const int ni = L.next_base + nb;
-      const NodeCfg nx = a.cfg[ni];
-      NodeCost nc{0.0, 0.0, 0.0, 0.0};
-      if (nx.d > 0) {
-        const double4 pc = a.pcost[nx.p];
-        nc.thr = a.thr_tab[a.thr_row[nx.p] + nx.d];
-        nc.pipe = pc.x;
-        nc.unit = pc.y;
-        nc.resume = pc.z;
-      }
+      const NodeCfg nx = STAGED ? s_cfg[ni] : a.cfg[ni];
+      const NodeCost nc = (STAGED && nb == static_cast<int>(blockIdx.x)) ? s_nc[j] : next_cost(nx);
       const PhiConst K = phi_const(L, S, nc);
       Cand best{0.0, 0.0, 0.0, 0.0, -1};
       // Prev nodes come in ascending P, descending D, so their bin counts
@@ -675,8 +746,8 @@ __global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScala
         if (pi >= L.prev_count) continue;
         (void)T2;
         const int gi = L.prev_base + pi;
-        const NodeCfg pv = a.cfg[gi];
-        const double* hp = histp + pv.hist_off;
+        const NodeCfg pv = STAGED ? s_cfg[gi] : a.cfg[gi];
+        const double* hp = STAGED ? s_prob + s_base[j] + pi * stride : histp + pv.hist_off;
         const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{hp}, a.thr_tab, a.thr_row, K);
         const double v = __dadd_rn(__ldcg(a.val + gi), ph.committed);
         const double mg = __dadd_rn(__ldcg(a.mig + gi), ph.mig);
@@ -708,7 +779,8 @@ __global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScala
       __syncthreads();
     }
     if (j < kTraceLevels) stamp(2 + 2 * j);
-    grid_barrier(a.barrier, epoch);
+    target += active;
+    grid_barrier(a.barrier, target);
     if (j < kTraceLevels) stamp(3 + 2 * j);
   }
 
@@ -770,24 +842,46 @@ __global__ void __launch_bounds__(256, 4) dp_persistent_kernel(DpArgs a, DpScala
   }
 }
 
+size_t dp_staged_smem(int n_nodes, int horizon, int n_prob) {
+  return StagedLayout{n_nodes, horizon, n_prob}.bytes();
+}
+
 cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStream_t st,
-                                 const DpArgs& a, const DpScalars& S) {
+                                 const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob) {
   if (a.horizon > kMaxHorizon) return cudaErrorInvalidValue;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_persistent_kernel, 256, 0);
+  const bool staged = n_prob >= 0;
+  const StagedLayout G{staged ? n_nodes : 0, staged ? a.horizon : 0, staged ? n_prob : 0};
+  const size_t smem = staged ? G.bytes() : 0;
+  void* fn = staged ? reinterpret_cast<void*>(dp_persistent_kernel<true>)
+                    : reinterpret_cast<void*>(dp_persistent_kernel<false>);
+  // occupancy per (device, variant, shared size): the grid must be co-resident
+  struct Occ {
+    int device = -1;
+    size_t smem = 0;
+    int per_sm = 0;
+  };
+  static thread_local Occ occ[2];
+  Occ& o = occ[staged ? 1 : 0];
+  cudaError_t e;
+  if (o.device != device || o.smem != smem) {
+    if (staged && smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.per_sm, fn, 256, smem);
     if (e != cudaSuccess) return e;
+    o.device = device;
+    o.smem = smem;
   }
-  (void)device;
-  const int cap = std::max(1, per_sm) * num_sms;
+  const int cap = std::max(1, o.per_sm) * num_sms;
   const int grid = std::max(1, std::min(cap, std::max(max_next, a.n_entries)));
-  cudaError_t e = cudaMemsetAsync(a.barrier, 0, sizeof(uint32_t), st);
+  e = cudaMemsetAsync(a.barrier, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   DpArgs aa = a;
   DpScalars ss = S;
-  void* params[] = {&aa, &ss};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dp_persistent_kernel), dim3(grid),
-                                     dim3(256), params, 0, st);
+  StagedLayout gg = G;
+  void* params[] = {&aa, &ss, &gg};
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), params, smem, st);
 }
 
 }  // namespace lp

@@ -84,11 +84,15 @@ struct DpArgs {
   double* final_value;
   uint32_t* barrier;
   int horizon;
+  int max_next;     // largest next-level node count: the blocks that run the levels
   uint64_t* trace;  // optional: per block, 2 * kTraceLevels + 2 globaltimer stamps
 };
 constexpr int kTraceLevels = 32;
 
+// n_prob >= 0: the shared-memory staged variant (small re-plans); n_prob =
+// sum over hist levels of prev_count * (min(k, n_now) + 1), n_nodes = all DP nodes.
 cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStream_t st,
-                                 const DpArgs& a, const DpScalars& S);
+                                 const DpArgs& a, const DpScalars& S, int n_nodes = 0, int n_prob = -1);
+size_t dp_staged_smem(int n_nodes, int horizon, int n_prob);
 
 }  // namespace lp

@@ -1,7 +1,8 @@
 """The execution modes of a re-plan must not change its result: one stage with
 the persistent DP kernel, three pipelined stages with per-level DP launches,
-one stage per ensemble, and the per-level launches alone all give the same
-plan (configs and FP64 step values, bit for bit).  The mode switches are read
+one stage per ensemble, the per-level launches alone (with and without
+programmatic dependent launch), and the persistent DP with and without its
+shared-memory staging of small re-plans all give the same plan (configs and FP64 step values, bit for bit).  The mode switches are read
 once per process, so each mode runs in a subprocess."""
 import json
 import os
@@ -48,5 +49,6 @@ def _run(env_extra):
 def test_execution_modes_agree():
     base = _run({"LIVEPUT_STAGES": "1"})  # one stage: persistent cooperative DP
     for env in ({"LIVEPUT_STAGES": "3"}, {"LIVEPUT_STAGES": "0"},
-                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"}):
+                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"},
+                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"}):
         assert _run(env) == base, env
