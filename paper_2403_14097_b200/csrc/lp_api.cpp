@@ -827,6 +827,7 @@ struct lp_handle {
   bool dp_launches = false;  // LIVEPUT_DP=launches: one kernel per level (A/B)
   bool dp_staged = true;     // LIVEPUT_DP_STAGED=0: never stage the DP in shared memory (A/B)
   int dp_staged_nprob = -1;  // >= 0: this re-plan's persistent DP runs staged
+  int dp_staged_kb = 100;    // shared-memory budget of the staged DP (LIVEPUT_DP_STAGED_KB)
   DevBuf tables, work;
   PinBuf pin_up, pin_down;
   size_t up_bytes = 0;
@@ -1096,6 +1097,7 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
     h->dp_launches = (e && std::string(e) == "launches");
     const char* es = getenv("LIVEPUT_DP_STAGED");
     h->dp_staged = !(es && es[0] == '0');
+    if (const char* ek = getenv("LIVEPUT_DP_STAGED_KB")) h->dp_staged_kb = std::max(0, std::min(200, atoi(ek)));
   }
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   *out = h;
@@ -1602,7 +1604,8 @@ lp_status prepare_dp(lp_handle* h) {
       if (L.has_hist) nprob += (long long)L.prev_count * (std::min(L.k, L.n_now) + 1);
     }
     const int n_nodes = h->levels[H - 1].next_base + h->levels[H - 1].next_count;
-    if (nprob < (1 << 20) && dp_staged_smem(n_nodes, H, (int)nprob) <= 40 * 1024) h->dp_staged_nprob = (int)nprob;
+    if (nprob < (1 << 20) && dp_staged_smem(n_nodes, H, (int)nprob) <= (size_t)h->dp_staged_kb * 1024)
+      h->dp_staged_nprob = (int)nprob;
   }
   size_t bytes = 0;
   lp_status us = upload_image(h,

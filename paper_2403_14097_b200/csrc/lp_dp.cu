@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "liveput.h"
@@ -864,7 +865,7 @@ cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStre
   Occ& o = occ[staged ? 1 : 0];
   cudaError_t e;
   if (o.device != device || o.smem != smem) {
-    if (staged && smem > 48 * 1024) {
+    if (staged) {  // the 48 KB default covers static + dynamic: always opt in
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) return e;
     }
@@ -873,8 +874,13 @@ cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStre
     o.device = device;
     o.smem = smem;
   }
-  const int cap = std::max(1, o.per_sm) * num_sms;
+  if (o.per_sm < 1)  // does not fit: the unstaged kernel needs no dynamic shared memory
+    return staged ? launch_dp_persistent(device, num_sms, max_next, st, a, S, 0, -1) : cudaErrorInvalidConfiguration;
+  const int cap = o.per_sm * num_sms;
   const int grid = std::max(1, std::min(cap, std::max(max_next, a.n_entries)));
+  if (getenv("LIVEPUT_DP_DEBUG"))
+    fprintf(stderr, "[dp] staged %d smem %zu per_sm %d grid %d max_next %d entries %d\n", (int)staged, smem,
+            o.per_sm, grid, max_next, a.n_entries);
   e = cudaMemsetAsync(a.barrier, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   DpArgs aa = a;

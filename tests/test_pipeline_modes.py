@@ -18,7 +18,7 @@ SCRIPT = r"""
 import json, sys
 sys.path.insert(0, %r)
 from bench import north_star_nseq
-from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_1p5b, lm_6p7b
+from paper_2403_14097_b200.model import CostTable, PlannerOptions, lm_1p5b, lm_6p7b, resnet152_dp
 from paper_2403_14097_b200.planner import Planner, reactive_plan
 out = []
 for w, ns, trials in [(lm_1p5b(), north_star_nseq(256, 24), 300000),
@@ -26,7 +26,9 @@ for w, ns, trials in [(lm_1p5b(), north_star_nseq(256, 24), 300000),
                       (lm_1p5b(), [77, 70, 71, 64, 69, 60], 50000),
                       (lm_1p5b(), [32, 28, 28, 26, 29, 26, 26, 21, 23, 23, 21, 25, 22], 10000),
                       (lm_1p5b(), [24, 20, 6, 3, 0, 9, 14, 20, 17], 10000),
-                      (lm_1p5b(), [40, 36, 37, 33, 30, 31, 26, 28, 24, 20, 22, 19, 21], 20000)]:
+                      (lm_1p5b(), [40, 36, 37, 33, 30, 31, 26, 28, 24, 20, 22, 19, 21], 20000),
+                      (resnet152_dp(), [35, 37, 36, 29, 27, 30, 33, 31, 28, 26, 30, 34, 36], 20000),
+                      (resnet152_dp(), [30, 28, 29, 27, 26, 24, 22, 23, 25, 27, 26, 24, 22], 20000)]:
     p = Planner(w, CostTable(), PlannerOptions(mc_trials=trials))
     plan = p.dp_optimize(reactive_plan(ns[0], w), ns, want_liveput=True)
     out.append([[s.config.pipelines if s.config else 0, s.config.stages if s.config else 0,

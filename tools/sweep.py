@@ -106,6 +106,28 @@ def run_cpu(trials, max_s):
     return out
 
 
+def summary(g6_path, g3_path, ref_path, md_path):
+    """Rewrite the table of profiles/sweep_summary.md from the three sweep files."""
+    g6 = {(r["n"], r["I"]): r for r in json.loads(Path(g6_path).read_text())}
+    g3 = {(r["n"], r["I"]): r for r in json.loads(Path(g3_path).read_text())}
+    rf = {(r["n"], r["I"]): r for r in json.loads(Path(ref_path).read_text())}
+    rows = ["| N | I | MC resolutions (1e6) | GPU (1e6) ms | GPU e2e ms | GPU (1e3) ms | ref (1e3) ms | ref/GPU at 1e3 |",
+            "|---|---|---|---|---|---|---|---|"]
+    for key in sorted(g6):
+        a, b, r = g6[key], g3.get(key, {}), rf.get(key, {})
+        ref_ms = r.get("ref_ms")
+        ratio = f"{ref_ms / b['device_ms']:.0f}×" if ref_ms and b.get("device_ms") else "—"
+        ref_s = f"{ref_ms:.0f}" if ref_ms else "skipped"
+        rows.append(f"| {key[0]} | {key[1]} | {a['resolutions']:.3g} | {a['device_ms']:.2f} | {a['e2e_ms']:.2f} | "
+                    f"{b.get('device_ms', float('nan')):.2f} | {ref_s} | {ratio} |")
+    md = Path(md_path).read_text().splitlines()
+    start = next(i for i, l in enumerate(md) if l.startswith("| N | I |"))
+    end = start
+    while end < len(md) and md[end].startswith("|"):
+        end += 1
+    Path(md_path).write_text("\n".join(md[:start] + rows + md[end:]) + "\n")
+
+
 def compare(a_path, b_path):
     a = {(r["n"], r["I"]): r for r in json.loads(Path(a_path).read_text())}
     b = {(r["n"], r["I"]): r for r in json.loads(Path(b_path).read_text())}
@@ -122,7 +144,7 @@ def compare(a_path, b_path):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["gpu", "cpu", "compare"])
+    ap.add_argument("mode", choices=["gpu", "cpu", "compare", "summary"])
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--max-s", type=float, default=60.0)
@@ -131,6 +153,8 @@ def main():
     a = ap.parse_args()
     if a.mode == "compare":
         sys.exit(1 if compare(*a.files) else 0)
+    if a.mode == "summary":  # gpu_1e6.json gpu_1e3.json ref_1e3.json summary.md
+        return summary(*a.files)
     res = run_gpu(a.trials, a.reps) if a.mode == "gpu" else run_cpu(a.trials, a.max_s)
     if a.out:
         Path(a.out).parent.mkdir(parents=True, exist_ok=True)
