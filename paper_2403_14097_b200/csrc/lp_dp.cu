@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "liveput.h"
 #include "lp_launch.h"
@@ -855,32 +856,42 @@ cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStre
   const size_t smem = staged ? G.bytes() : 0;
   void* fn = staged ? reinterpret_cast<void*>(dp_persistent_kernel<true>)
                     : reinterpret_cast<void*>(dp_persistent_kernel<false>);
-  // occupancy per (device, variant, shared size): the grid must be co-resident
+  // occupancy per (device, variant, shared size): the grid must be co-resident.
+  // The staged variant's shared size changes with every re-plan, so the
+  // opt-in above 48 KB (static + dynamic) is set once at the largest size and
+  // the occupancy answers are memoised per 1 KB bucket.
   struct Occ {
     int device = -1;
-    size_t smem = 0;
-    int per_sm = 0;
+    std::vector<int> per_sm;  // by ceil(smem / 1 KB); 0: unknown
   };
   static thread_local Occ occ[2];
   Occ& o = occ[staged ? 1 : 0];
   cudaError_t e;
-  if (o.device != device || o.smem != smem) {
-    if (staged) {  // the 48 KB default covers static + dynamic: always opt in
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (o.device != device) {
+    if (staged) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       if (e != cudaSuccess) return e;
     }
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.per_sm, fn, 256, smem);
-    if (e != cudaSuccess) return e;
     o.device = device;
-    o.smem = smem;
+    o.per_sm.assign(201, 0);
   }
-  if (o.per_sm < 1)  // does not fit: the unstaged kernel needs no dynamic shared memory
+  const size_t bucket = (smem + 1023) / 1024;
+  if (bucket > 200) return launch_dp_persistent(device, num_sms, max_next, st, a, S, 0, -1);
+  int& per_sm = o.per_sm[bucket];
+  if (per_sm == 0) {
+    int v = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, fn, 256, bucket * 1024);
+    if (e != cudaSuccess) return e;
+    per_sm = v > 0 ? v : -1;
+  }
+  if (per_sm < 1)  // does not fit: the unstaged kernel needs no dynamic shared memory
     return staged ? launch_dp_persistent(device, num_sms, max_next, st, a, S, 0, -1) : cudaErrorInvalidConfiguration;
-  const int cap = o.per_sm * num_sms;
+  const int cap = per_sm * num_sms;
   const int grid = std::max(1, std::min(cap, std::max(max_next, a.n_entries)));
-  if (getenv("LIVEPUT_DP_DEBUG"))
+  static const bool debug = getenv("LIVEPUT_DP_DEBUG") != nullptr;
+  if (debug)
     fprintf(stderr, "[dp] staged %d smem %zu per_sm %d grid %d max_next %d entries %d\n", (int)staged, smem,
-            o.per_sm, grid, max_next, a.n_entries);
+            per_sm, grid, max_next, a.n_entries);
   e = cudaMemsetAsync(a.barrier, 0, sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   DpArgs aa = a;
