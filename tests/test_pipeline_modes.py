@@ -2,7 +2,8 @@
 the persistent DP kernel, three pipelined stages with per-level DP launches,
 one stage per ensemble, the per-level launches alone (with and without
 programmatic dependent launch), and the persistent DP with and without its
-shared-memory staging of small re-plans all give the same plan (configs and FP64 step values, bit for bit).  The mode switches are read
+shared-memory staging of small re-plans, other DP block and work-item sizes,
+and the alternative histogram kernels all give the same plan (configs and FP64 step values, bit for bit).  The mode switches are read
 once per process, so each mode runs in a subprocess."""
 import json
 import os
@@ -52,5 +53,8 @@ def test_execution_modes_agree():
     base = _run({"LIVEPUT_STAGES": "1"})  # one stage: persistent cooperative DP
     for env in ({"LIVEPUT_STAGES": "3"}, {"LIVEPUT_STAGES": "0"},
                 {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"},
-                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"}):
+                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"},
+                {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
+                {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"},
+                {"LIVEPUT_HIST_KERNEL": "norows"}):
         assert _run(env) == base, env
