@@ -25,7 +25,8 @@ def main():
     w = lm_1p5b()
     ok = True
     for name, ns, trials in [("bench", north_star_nseq(256, 24), 1_000_000), ("predict", PREDICT, 1_000_000),
-                             ("odd", [77, 70, 71, 64, 69, 60], 12_345)]:
+                             ("odd", [77, 70, 71, 64, 69, 60], 12_345),
+                             ("n32", [32, 28, 28, 26, 29, 26, 26, 21, 23, 23, 21, 25, 22], 10_000)]:
         opt = PlannerOptions(mc_trials=trials)
         cur = reactive_plan(ns[0], w)
         p = Planner(w, CostTable(), opt, device=local)
