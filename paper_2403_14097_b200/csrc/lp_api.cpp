@@ -44,6 +44,30 @@ constexpr int kIncMaxK = 8;                     // incidence kernel up to k = 8,
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// Row-kernel block shape: threads per block cap, shared-memory budget per
+// block and the entries + event-table share of it. LIVEPUT_ROWS_SHAPE =
+// "T,smem_kb,fixed_kb" overrides the defaults (256, 112, 64) for A/B runs.
+struct RowsShape {
+  int tmax = 256;
+  size_t smem = kSmemBudgetScn;
+  size_t fixed = kScnFixedBudget;
+};
+const RowsShape& rows_shape() {
+  static const RowsShape s = [] {
+    RowsShape r;
+    if (const char* e = getenv("LIVEPUT_ROWS_SHAPE")) {
+      int t = 0, sk = 0, fk = 0;
+      if (sscanf(e, "%d,%d,%d", &t, &sk, &fk) == 3 && t >= 32 && t <= 256 && sk > 0 && fk > 0 && fk <= sk) {
+        r.tmax = t & ~31;
+        r.smem = (size_t)sk * 1024;
+        r.fixed = (size_t)fk * 1024;
+      }
+    }
+    return r;
+  }();
+  return s;
+}
+
 // ---------------------------------------------------------------------------
 // growable device / pinned host buffers
 struct DevBuf {
@@ -410,6 +434,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512) {
       // bit-sliced row kernel (lp_hist_rows.cu)
       const int kreg = pd.k <= kMaxKReg ? 16 : 0;
+      const RowsShape& rs = rows_shape();
       int e = pd.entry_base;
       while (e < e_end) {
         int e2 = e;
@@ -417,7 +442,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (e2 < e_end) {
           const EntryDesc& x = hp.entries[e2];
           const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
-          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(2 * (size_t)ev2) > kScnFixedBudget)
+          if (e2 > e && a16(sizeof(EntryDesc) * (e2 - e + 1)) + a16(2 * (size_t)ev2) > rs.fixed)
             break;
           ev = ev2;
           ++e2;
@@ -426,9 +451,9 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         int pmax_res = 0;
         while (e_res < e2 && hp.entries[e_res].tmax >= 2) pmax_res = std::max(pmax_res, hp.entries[e_res++].P);
         const int wmax = pmax_res <= 128 ? 4 : 8;
-        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(2 * (size_t)ev) <= kScnFixedBudget;
-        int T = 256;
-        while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact) > kSmemBudgetScn)
+        const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(2 * (size_t)ev) <= rs.fixed;
+        int T = rs.tmax;
+        while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact) > rs.smem)
           T -= 32;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
