@@ -2,7 +2,8 @@
 the persistent DP kernel, three pipelined stages with per-level DP launches,
 one stage per ensemble, the per-level launches alone (with and without
 programmatic dependent launch), and the persistent DP with and without its
-shared-memory staging of small re-plans, other DP block and work-item sizes,
+shared-memory staging of small re-plans, other DP block and work-item sizes, other row-kernel block shapes
+(small event tables split a pair's depths over many work items),
 and the alternative histogram kernels all give the same plan (configs and FP64 step values, bit for bit).  The mode switches are read
 once per process, so each mode runs in a subprocess."""
 import json
@@ -56,5 +57,6 @@ def test_execution_modes_agree():
                 {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"},
                 {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
                 {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"},
-                {"LIVEPUT_HIST_KERNEL": "norows"}):
+                {"LIVEPUT_HIST_KERNEL": "norows"}, {"LIVEPUT_ROWS_SHAPE": "160,56,8"},
+                {"LIVEPUT_ROWS_SHAPE": "96,40,2"}):
         assert _run(env) == base, env
