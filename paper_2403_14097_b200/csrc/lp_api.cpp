@@ -51,6 +51,7 @@ struct RowsShape {
   int tmax = 256;
   size_t smem = kSmemBudgetScn;
   size_t fixed = kScnFixedBudget;
+  int kreg_max = kMaxKReg;  // LIVEPUT_ROWS_KREG=0: byte-table draws for every k
 };
 const RowsShape& rows_shape() {
   static const RowsShape s = [] {
@@ -63,6 +64,7 @@ const RowsShape& rows_shape() {
         r.fixed = (size_t)fk * 1024;
       }
     }
+    if (const char* e = getenv("LIVEPUT_ROWS_KREG")) r.kreg_max = atoi(e) == 0 ? 0 : kMaxKReg;
     return r;
   }();
   return s;
@@ -433,8 +435,8 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     const int e_end = pd.entry_base + pd.n_entries;
     if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512) {
       // bit-sliced row kernel (lp_hist_rows.cu)
-      const int kreg = pd.k <= kMaxKReg ? 16 : 0;
       const RowsShape& rs = rows_shape();
+      const int kreg = pd.k <= rs.kreg_max ? 16 : 0;
       int e = pd.entry_base;
       while (e < e_end) {
         int e2 = e;

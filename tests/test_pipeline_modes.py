@@ -58,5 +58,5 @@ def test_execution_modes_agree():
                 {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
                 {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"},
                 {"LIVEPUT_HIST_KERNEL": "norows"}, {"LIVEPUT_ROWS_SHAPE": "160,56,8"},
-                {"LIVEPUT_ROWS_SHAPE": "96,40,2"}):
+                {"LIVEPUT_ROWS_SHAPE": "96,40,2"}, {"LIVEPUT_ROWS_KREG": "0"}):
         assert _run(env) == base, env

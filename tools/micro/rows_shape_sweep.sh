@@ -5,7 +5,12 @@ out=${1:-gpurun_out/rows_shape_sweep.log}
 : > "$out"
 for rep in 1 2; do
   for shape in ${SHAPES:-default 224,74,52 192,74,56 160,56,40 128,56,40 224,74,40}; do
-    if [ "$shape" = default ]; then unset LIVEPUT_ROWS_SHAPE; else export LIVEPUT_ROWS_SHAPE=$shape; fi
+    unset LIVEPUT_ROWS_SHAPE LIVEPUT_ROWS_KREG
+    case "$shape" in
+      default) ;;
+      kreg0) export LIVEPUT_ROWS_KREG=0 ;;
+      *) export LIVEPUT_ROWS_SHAPE=$shape ;;
+    esac
     line=$(timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1)
     python - "$shape" "$line" >> "$out" <<'PY'
 import json, sys, hashlib
