@@ -211,6 +211,12 @@ lp_status lp_dump_scenarios(lp_handle* h, int32_t n, int32_t n_minus, int32_t tr
 lp_status lp_nccl_unique_id(uint8_t out[LP_NCCL_ID_BYTES]);
 lp_status lp_comm_init(lp_handle* h, const uint8_t id[LP_NCCL_ID_BYTES], int32_t nranks,
                        int32_t rank);
+/* Parity mode of the split: lp_survivor_hist then counts only trial slice
+ * [count*rank/nranks, count*(rank+1)/nranks) of the ensemble (the slice rank
+ * `rank` of an nranks-GPU re-plan generates) and *total is the slice size.
+ * Summing the slices of every rank reproduces the single-GPU counts.  The
+ * re-plan path is unaffected (it follows lp_comm_init). */
+lp_status lp_set_shard(lp_handle* h, int32_t rank, int32_t nranks);
 
 /* ---- host table producers (perf_model stays on the host):
  *      throughput perf_model.cpp:14-42, enumerate_configs :44-52,

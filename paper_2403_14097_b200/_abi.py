@@ -182,6 +182,7 @@ _SIGS = {
     "lp_dump_scenarios": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, _P(C.c_uint16)]),
     "lp_nccl_unique_id": (C.c_int, [_P(C.c_uint8)]),
     "lp_comm_init": (C.c_int, [C.c_void_p, _P(C.c_uint8), C.c_int32, C.c_int32]),
+    "lp_set_shard": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "lp_throughput": (C.c_double, [_P(lp_profile), lp_config]),
     "lp_depth_feasible": (C.c_int32, [_P(lp_profile), C.c_int32]),
     "lp_enumerate_configs": (C.c_int32, [_P(lp_profile), C.c_int32, _P(lp_config), C.c_int32]),

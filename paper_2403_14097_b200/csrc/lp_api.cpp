@@ -829,6 +829,7 @@ struct lp_handle {
   std::string err;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  int shard_rank = 0, shard_n = 1;  // lp_set_shard: survivor_hist on one trial slice
 
   // re-plan state
   bool prepared = false;
@@ -1002,17 +1003,21 @@ lp_status planner_rows(lp_handle* h, int D, int P, int n, int k, std::vector<uin
   EnsembleSpec sp;
   lp_status s = planner_spec(h, n, k, sp);
   if (s != LP_OK) return s;
-  *total = sp.count;
+  const uint64_t t_lo = sp.count * (uint64_t)h->shard_rank / (uint64_t)h->shard_n;
+  const uint64_t t_hi = sp.count * (uint64_t)(h->shard_rank + 1) / (uint64_t)h->shard_n;
+  *total = t_hi - t_lo;
   auto key = std::make_tuple(n, k, P);
   auto it = h->hist_cache.find(key);
   if (it == h->hist_cache.end() || it->second.first < D) {
     const int Dm = n / P;  // every D of this depth at once
     sp.dmax_by_p[P] = std::max(Dm, D);
     std::vector<uint32_t> all;
-    // fetch all rows of the entry: run and copy D = 1..Dm
+    // fetch all rows of the entry: run and copy D = 1..Dm.  With a shard
+    // set this is the rank's slice of the multi-GPU split (build_hist_plan's
+    // t_lo / t_hi, finalize with the local ensemble size).
     HistPlan hp;
     std::string err;
-    s = build_hist_plan({sp}, 0, 1, hp, err);
+    s = build_hist_plan({sp}, h->shard_rank, h->shard_n, hp, err);
     if (s != LP_OK) return fail(h, s, "%s", err.c_str());
     Packer pk;
     HistDev d{};
@@ -1306,8 +1311,12 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     const int si = it->second;
     EnsembleSpec& sp = specs[si];
     if (j == 0) {
+      // Dmax = floor(n / P) like every full-level entry (not current.pipelines):
+      // the kernels resolve t >= 2 events only over the prefix of entries with
+      // tmax >= 2, so Dmax must stay non-increasing in P even when current's
+      // depth is infeasible and sorts below every feasible one.
       int& dm = sp.dmax_by_p[current.stages];
-      dm = std::max(dm, current.pipelines);
+      dm = std::max(dm, std::max(current.pipelines, n_now / current.stages));
       spec_cur[si] = {current.pipelines, current.stages};
     } else if (!spec_full[si]) {
       spec_full[si] = 1;
@@ -1479,6 +1488,8 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
       h->store_used += hist_row(E.Dmax + 1, pd.k);
     }
   }
+  if (h->store_used > (size_t)INT32_MAX)
+    return fail(h, LP_EUNSUPPORTED, "histogram store exceeds 2^31 probabilities");
   {
     lp_status gs = grow_store(h, h->store_used);
     if (gs != LP_OK) return gs;
@@ -1914,7 +1925,8 @@ lp_status lp_replan(lp_handle* h, lp_config current, const int32_t* n_seq, int32
 lp_status lp_set_hist_cache(lp_handle* h, int32_t enable, uint64_t max_bytes) {
   if (!h) return fail(nullptr, LP_EINVAL, "null handle");
   h->cache_on = enable != 0;
-  h->cache_max = max_bytes ? max_bytes : (4ull << 30);
+  // store offsets are int32 element indices (EntryDesc / store_off)
+  h->cache_max = std::min<uint64_t>(max_bytes ? max_bytes : (4ull << 30), (uint64_t)INT32_MAX * 8ull);
   h->store_idx.clear();
   h->store_used = 0;
   h->prepared = false;
@@ -1978,6 +1990,7 @@ lp_status lp_cache_export(lp_handle* h, void* buf, uint64_t cap, uint64_t* len) 
   if (!buf) return LP_OK;
   if (cap < need) return fail(h, LP_EINVAL, "lp_cache_export: buffer of %llu bytes, need %llu",
                               (unsigned long long)cap, (unsigned long long)need);
+  cudaSetDevice(h->device);
   LP_CUDA(h, cudaStreamSynchronize(h->stream));
   unsigned char* o = static_cast<unsigned char*>(buf);
   CacheHeader ch{kCacheMagic, h->opt.mc_trials, h->opt.exact_cap, h->opt.mc_seed,
@@ -2013,6 +2026,7 @@ lp_status lp_cache_import(lp_handle* h, const void* buf, uint64_t len) {
       ch.mc_seed != h->opt.mc_seed)
     return fail(h, LP_EINVAL, "lp_cache_import: table was sampled with different PlannerOptions "
                               "(mc_trials/exact_cap/mc_seed)");
+  cudaSetDevice(h->device);
   h->cache_on = true;
   for (uint64_t s = 0; s < ch.slots; ++s) {
     if (p + sizeof(SlotHeader) > end) return fail(h, LP_EINVAL, "lp_cache_import: truncated");
@@ -2028,6 +2042,8 @@ lp_status lp_cache_import(lp_handle* h, const void* buf, uint64_t len) {
       p += sizeof eh;
       if (eh.len != hist_row(eh.Dmax + 1, sh.k) || p + sizeof(double) * eh.len > end)
         return fail(h, LP_EINVAL, "lp_cache_import: corrupt entry");
+      if (h->store_used + eh.len > (size_t)INT32_MAX)
+        return fail(h, LP_EUNSUPPORTED, "lp_cache_import: table exceeds 2^31 probabilities");
       lp_status gs = grow_store(h, h->store_used + eh.len);
       if (gs != LP_OK) return gs;
       LP_CUDA(h, cudaMemcpy(static_cast<double*>(h->store.p) + h->store_used, p,
@@ -2284,6 +2300,14 @@ lp_status lp_nccl_unique_id(uint8_t out[LP_NCCL_ID_BYTES]) {
   return LP_OK;
 }
 
+lp_status lp_set_shard(lp_handle* h, int32_t rank, int32_t nranks) {
+  if (!h || nranks < 1 || rank < 0 || rank >= nranks) return fail(h, LP_EINVAL, "lp_set_shard: bad argument");
+  h->shard_rank = rank;
+  h->shard_n = nranks;
+  h->hist_cache.clear();
+  return LP_OK;
+}
+
 lp_status lp_comm_init(lp_handle* h, const uint8_t id[LP_NCCL_ID_BYTES], int32_t nranks,
                        int32_t rank) {
   if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks)
@@ -2300,6 +2324,13 @@ lp_status lp_comm_init(lp_handle* h, const uint8_t id[LP_NCCL_ID_BYTES], int32_t
     ncclResult_t r = nccl().CommInitRank(&h->comm, nranks, uid, rank);
     if (r != ncclSuccess)
       return fail(h, LP_ENCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+    // NCCL connects its channels lazily on the first collective (0.4-0.75 s
+    // measured on B200); pay that here, not inside the first re-plan.
+    LP_CUDA(h, h->work.ensure(256));
+    r = nccl().AllReduce(h->work.p, h->work.p, 1, ncclUint32, ncclSum, h->comm, h->stream);
+    if (r != ncclSuccess)
+      return fail(h, LP_ENCCL, "ncclAllReduce (warm-up): %s", nccl().GetErrorString(r));
+    LP_CUDA(h, cudaStreamSynchronize(h->stream));
   }
   h->nranks = nranks;
   h->rank = rank;

@@ -25,6 +25,7 @@
 #include <stdint.h>
 
 #include "lp_device.cuh"
+#include "lp_launch.h"
 #include "lp_layout.h"
 
 namespace lp {
@@ -356,8 +357,7 @@ static cudaError_t launch_regs(int blocks, size_t smem, cudaStream_t st, const W
                                const PairDesc* pairs, const EntryDesc* ents, const DrawConst* dr,
                                const uint64_t* binom, uint32_t* evt, uint32_t* h0) {
   auto fn = hist_regs_kernel<KMAX, SM>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, 256, smem, st>>>(w, pairs, ents, dr, binom, evt, h0);
   return cudaGetLastError();
@@ -385,8 +385,7 @@ cudaError_t launch_hist_ctr(bool smem_evt, int blocks, int threads, size_t smem,
                             uint32_t* evt, uint32_t* h0) {
   if (blocks <= 0) return cudaSuccess;
   auto fn = smem_evt ? hist_ctr_kernel<true> : hist_ctr_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, evt, h0, pmax_cap);
   return cudaGetLastError();

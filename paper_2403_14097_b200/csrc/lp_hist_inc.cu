@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "lp_device.cuh"
+#include "lp_launch.h"
 #include "lp_layout.h"
 
 namespace lp {
@@ -154,8 +155,7 @@ static cudaError_t launch_inc_t(int blocks, int threads, size_t smem, cudaStream
                                 const DrawConst* dr, const uint64_t* binom, const uint16_t* divtab,
                                 uint32_t* evt, uint32_t* h0) {
   auto fn = hist_inc_kernel<KMAX, SM>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, divtab, evt, h0);
   return cudaGetLastError();

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "lp_device.cuh"
+#include "lp_launch.h"
 #include "lp_layout.h"
 
 namespace lp {
@@ -559,8 +560,7 @@ static cudaError_t launch_rows_t(int blocks, int threads, size_t smem, cudaStrea
                                  const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
                                  uint32_t* h0) {
   auto fn = hist_rows_kernel<KREG, WMAX, SM>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, evt, h0);
   return cudaGetLastError();

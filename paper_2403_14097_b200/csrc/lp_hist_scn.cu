@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include "lp_device.cuh"
+#include "lp_launch.h"
 #include "lp_layout.h"
 
 namespace lp {
@@ -193,8 +194,7 @@ static cudaError_t launch_scn_t(int blocks, int threads, size_t smem, int uw, cu
                                 const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
                                 uint32_t* h0) {
   auto fn = hist_scn_kernel<KREG, SM>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, evt, h0, uw);
   return cudaGetLastError();

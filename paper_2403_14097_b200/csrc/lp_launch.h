@@ -8,6 +8,9 @@
 
 namespace lp {
 
+// Raise a kernel's dynamic shared-memory opt-in once per (device, kernel).
+cudaError_t smem_optin(const void* fn, size_t smem);
+
 cudaError_t launch_hist_regs(int kmax, bool smem_evt, int blocks, size_t smem, cudaStream_t st,
                              const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
                              const DrawConst* dr, const uint64_t* binom, uint32_t* evt,

@@ -191,6 +191,11 @@ class Planner:
         arr = (C.c_uint8 * _abi.LP_NCCL_ID_BYTES).from_buffer_copy(uid)
         _abi.check(self._lib.lp_comm_init(self._h, arr, nranks, rank), self._h)
 
+    def set_shard(self, rank: int, nranks: int) -> None:
+        """survivor_counts over trial slice `rank` of an `nranks`-way split
+        (parity mode of the multi-GPU decomposition; lp_set_shard)."""
+        _abi.check(self._lib.lp_set_shard(self._h, rank, nranks), self._h)
+
     # ---- host table producers -----------------------------------------
     def configs(self, n: int) -> List[ParallelConfig]:
         return enumerate_configs(n, self.w)

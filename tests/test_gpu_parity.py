@@ -388,3 +388,76 @@ def test_offline_tables_roundtrip():
         c.import_tables(blob)
     for p in (a, b, c):
         p.close()
+
+
+def _decode_tables(blob):
+    """lp_cache_export layout (lp_api.cpp CacheHeader / SlotHeader / EntryHeader):
+    yields (n, k, count, P, Dmax, probabilities by D: list of min(k,D)+1 by deficit)."""
+    import struct
+    magic, trials, cap, seed, slots = struct.unpack_from("<IiQQQ", blob, 0)
+    assert magic == 0x3143504C
+    o = 32
+    for _ in range(slots):
+        n, k, count, ents, _pad = struct.unpack_from("<iiQii", blob, o)
+        o += 24
+        for _ in range(ents):
+            P, dmax, ln = struct.unpack_from("<iiq", blob, o)
+            o += 16
+            vals = struct.unpack_from(f"<{ln}d", blob, o)
+            o += 8 * ln
+            rows, i = [], 0
+            for D in range(1, dmax + 1):
+                w = min(k, D) + 1
+                rows.append(vals[i:i + w])
+                i += w
+            assert i == ln
+            yield n, k, count, P, dmax, rows
+    assert o == len(blob)
+
+
+def test_offline_tables_match_oracle():
+    """SURVEY §8f #2 pinned to the oracle: every exported probability
+    p(n, k, D, P, m) equals the oracle's count_m / count bit for bit
+    (optimizer.cpp:92 normalisation), and a re-plan served from the imported
+    tables equals the oracle's plan."""
+    w = lm_1p5b()
+    opt = PlannerOptions(mc_trials=7000)
+    ns = [80, 74, 74, 70, 73, 66]
+    pairs = sorted({(ns[j], max(0, ns[j] - ns[j + 1])) for j in range(len(ns) - 1)})
+    a = planner(w, opt)
+    a.precompute(pairs)
+    blob = a.export_tables()
+    seen = set()
+    for n, k, count, P, dmax, rows in _decode_tables(blob):
+        seen.add((n, k))
+        exact = O.oracle_lib().or_scenario_count(n, k) <= opt.exact_cap
+        cfgs = [ParallelConfig(D, P) for D in range(1, dmax + 1)]
+        counts, tot = O.oracle_ensemble_counts(n, k, exact, opt.mc_trials, O.planner_seed(0x5EED, n, k), cfgs)
+        assert tot == count
+        for D, row in zip(range(1, dmax + 1), rows):
+            want = [float(counts[D - 1][D - d]) / float(tot) for d in range(min(k, D) + 1)]
+            assert [x.hex() for x in row] == [x.hex() for x in want], (n, k, D, P)
+    assert seen == set(pairs)
+    b = planner(w, opt)
+    b.import_tables(blob)
+    cur = ParallelConfig(10, 8)
+    got = plan_rows(b.dp_optimize(cur, ns))
+    assert got == plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns))
+    a.close()
+    b.close()
+
+
+def test_infeasible_current_depth_keeps_later_levels():
+    """a level-0 `current` at a depth below the feasible minimum
+    (P=3 < 7 for lm_1p5b) with D=1, whose (n, k) ensemble is also read by a
+    later level: every feasible depth must keep its t >= 2 events."""
+    w = lm_1p5b()
+    opt = PlannerOptions(mc_trials=20000)
+    for cur, ns in [(ParallelConfig(1, 3), [64, 56, 64, 56, 64, 56]),
+                    (ParallelConfig(2, 5), [96, 84, 90, 96, 84, 80]),
+                    (ParallelConfig(1, 1), [48, 40, 48, 40])]:
+        p = planner(w, opt)
+        got = plan_rows(p.dp_optimize(cur, ns))
+        ref = plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns))
+        assert got == ref, (cur, ns)
+        p.close()
