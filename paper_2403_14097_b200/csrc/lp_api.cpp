@@ -41,6 +41,7 @@ constexpr size_t kScnFixedBudget = 64 * 1024;   // entries + event table per blo
 constexpr size_t kSmemBudgetScn = 112 * 1024;   // two blocks per SM
 constexpr size_t kSmemBudgetInc = 75 * 1024;    // three blocks per SM
 constexpr int kIncMaxK = 8;                     // incidence kernel up to k = 8, rows above
+constexpr size_t kSmemBudgetBits = 48 * 1024;   // bits kernel: four 256-thread blocks per SM
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -210,6 +211,7 @@ struct HistPlan {
   std::vector<uint64_t> binom;
   std::vector<WorkItem> work;
   std::vector<uint16_t> divtab;
+  std::vector<uint32_t> dmask;  // bits kernel: per (range, pass, d) depth-divisor masks
   std::vector<Group> groups;
   // Pipeline stages: pairs (and so entries, hist rows) are contiguous per
   // stage, in the order the DP first reads them.
@@ -266,6 +268,29 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
     if (ents[e].P >= 2)
       for (int d = ents[e].P; d < n; d += ents[e].P)
         out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
+}
+
+// Must match the carve in hist_bits_kernel (lp_hist_bits.cu).
+size_t smem_bits(int nbits, int kmax, int n, int64_t evt_len, bool smem_evt, int npass, int ng) {
+  return a16(16 * (size_t)std::max(nbits, 1)) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
+         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (size_t)npass * n * ng);
+}
+
+// Divisor masks of the bits kernel: word (pass, d, g) has bit b set when
+// the resolution depth pass*32*ng + g*32 + b divides d (d >= 1).  Appended to
+// `out` at a 4-word boundary; returns the offset.
+int build_dmask(const std::vector<EntryDesc>& ents, int eb0, int nres, int n, int ng, int npass,
+                std::vector<uint32_t>& out) {
+  while (out.size() % 4) out.push_back(0u);
+  const int off = (int)out.size();
+  out.resize(out.size() + (size_t)npass * n * ng, 0u);
+  for (int i = 0; i < nres; ++i) {
+    const int P = ents[eb0 + i].P;
+    const int ps = i / (32 * ng), g = (i / 32) % ng, b = i % 32;
+    uint32_t* tab = out.data() + off + (size_t)ps * n * ng;
+    for (int d = P; d < n; d += P) tab[(size_t)d * ng + g] |= 1u << b;
+  }
+  return off;
 }
 
 // Must match the carve in hist_rows_kernel (lp_hist_rows.cu).
@@ -428,6 +453,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   const bool legacy = kenv && std::string(kenv) == "legacy";
   const bool inc_off = kenv && std::string(kenv) == "noinc";
   const bool rows_off = kenv && std::string(kenv) == "norows";
+  const bool bits_off = kenv && (std::string(kenv) == "inc" || std::string(kenv) == "noinc");
   for (int pi = 0; pi < (int)hp.pairs.size(); ++pi) {
     const PairDesc& pd = hp.pairs[pi];
     const uint64_t local = pd.t_hi - pd.t_lo;
@@ -470,6 +496,61 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
           gv1.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, 0});
+        }
+        e = e2;
+      }
+      continue;
+    }
+    if (!legacy && pd.k <= kIncMaxK && !bits_off) {
+      // bit-parallel incidence kernel (lp_hist_bits.cu)
+      const int km = pd.k <= 4 ? 4 : 8;
+      int e = pd.entry_base;
+      auto shape = [&](int e0, int e1, int64_t ev, bool sm, int* nres_o, int* ng_o, int* np_o) {
+        const int eb0 = (e0 < e1 && hp.entries[e0].P == 1) ? e0 + 1 : e0;
+        int nres = 0;
+        while (eb0 + nres < e1 && hp.entries[eb0 + nres].tmax >= 2) ++nres;
+        const int ng = nres <= 32 ? 1 : (nres <= 64 ? 2 : 4);
+        const int np = (nres + 32 * ng - 1) / (32 * ng);
+        *nres_o = nres;
+        *ng_o = ng;
+        *np_o = np;
+        return smem_bits(np * 32 * ng, km, pd.n, ev, sm, np, ng);
+      };
+      while (e < e_end) {
+        int e2 = e;
+        int64_t ev = 0;
+        int nres, ng, np;
+        while (e2 < e_end) {
+          const EntryDesc& x = hp.entries[e2];
+          const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
+          if (e2 > e && x.tmax >= 2 && shape(e, e2 + 1, ev2, true, &nres, &ng, &np) > kSmemBudgetBits) break;
+          ev = ev2;
+          ++e2;
+        }
+        const size_t sm_need = shape(e, e2, ev, true, &nres, &ng, &np);
+        if (nres == 0 && e != pd.entry_base && !(hp.entries[e].P == 1 && hp.entries[e].tmax >= 2)) {
+          e = e2;  // nothing to resolve and not the h0 owner
+          continue;
+        }
+        const bool sm = sm_need <= kSmemBudgetBits;
+        const size_t smem = shape(e, e2, ev, sm, &nres, &ng, &np);
+        const int eb0 = (hp.entries[e].P == 1) ? e + 1 : e;
+        const int doff = build_dmask(hp.entries, eb0, nres, pd.n, ng, np, hp.dmask);
+        const int T = 256;
+        const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
+        auto& gv5 = groups[{specs[pi].stage, 5, km * 16 + ng, T, sm ? 1 : 0}];
+        {
+          WorkItem w{};
+          w.pair = pi;
+          w.e_lo = e;
+          w.e_hi = e2;
+          w.e_res_hi = eb0 + nres;
+          w.evt_lo = hp.entries[e].evt_off;
+          w.evt_len = (int)ev;
+          w.smem_evt = sm ? 1 : 0;
+          w.dtab_off = doff;
+          w.dtab_len = np;
+          gv5.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, 0});
         }
         e = e2;
       }
@@ -683,6 +764,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
 
 struct HistDev {
   const uint16_t* divtab;
+  const uint32_t* dmask;
   const PairDesc* pairs;
   const EntryDesc* entries;
   const DrawConst* draws;
@@ -703,7 +785,10 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   if (e != cudaSuccess) return e;
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 4)
+    if (g.kind == 5)
+      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+                           d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
+    else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0);
     else if (g.kind == 3)
@@ -734,7 +819,10 @@ cudaError_t run_hist_stage(const HistPlan& hp, const HistDev& d, cudaStream_t st
   for (const Group& g : hp.groups) {
     if (g.stage != stage) continue;
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 4)
+    if (g.kind == 5)
+      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+                           d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
+    else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0);
     else if (g.kind == 3)
@@ -845,7 +933,7 @@ struct lp_handle {
   std::vector<DenseMap<int>> level_depths;
   ThrTable thr;
   DpScalars S{};
-  size_t off_divtab = 0;
+  size_t off_divtab = 0, off_dmask = 0;
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
@@ -924,7 +1012,8 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
                       Packer& pk, std::vector<size_t>& extra_offs) {
   (void)extra_offs;
   const size_t op = pk.add(hp.pairs), oe = pk.add(hp.entries), od = pk.add(hp.draws),
-               ob = pk.add(hp.binom), ow = pk.add(hp.work), odt = pk.add(hp.divtab);
+               ob = pk.add(hp.binom), ow = pk.add(hp.work), odt = pk.add(hp.divtab),
+               odm = pk.add(hp.dmask);
   LP_CUDA(h, tables.ensure(pk.bytes.size()));
   LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
   std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
@@ -939,6 +1028,7 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
   d.binom = dptr<uint64_t>(tables, ob);
   d.work = dptr<WorkItem>(tables, ow);
   d.divtab = dptr<uint16_t>(tables, odt);
+  d.dmask = dptr<uint32_t>(tables, odm);
   d.evt = dptr<uint32_t>(work, 0);
   d.h0 = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)));
   d.hist = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)) +
@@ -1501,6 +1591,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
                                 {sec(h->hp.pairs, &h->off_pairs), sec(h->hp.entries, &h->off_entries),
                                  sec(h->hp.draws, &h->off_draws), sec(h->hp.binom, &h->off_binom),
                                  sec(h->hp.work, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
+                                 sec(h->hp.dmask, &h->off_dmask),
                                  sec(h->store_off, &h->off_store_off)},
                                 h->tables, h->pin_up, h->ev_up[0], &bytes, h->stream);
     if (us != LP_OK) return us;
@@ -1672,6 +1763,7 @@ lp_status exec_hist(lp_handle* h) {
   d.binom = dptr<uint64_t>(h->tables, h->off_binom);
   d.work = dptr<WorkItem>(h->tables, h->off_work);
   d.divtab = dptr<uint16_t>(h->tables, h->off_divtab);
+  d.dmask = dptr<uint32_t>(h->tables, h->off_dmask);
   d.evt = dptr<uint32_t>(h->work, h->w_evt);
   d.h0 = dptr<uint32_t>(h->work, h->w_h0);
   d.hist = dptr<uint32_t>(h->work, h->w_hist);
