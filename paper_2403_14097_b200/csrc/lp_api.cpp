@@ -270,10 +270,20 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
         out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
 }
 
+// LIVEPUT_BITS=rows selects the row-parallel variant of the bits kernel (A/B)
+bool bits_gseq() {
+  static const bool v = [] {
+    const char* e = getenv("LIVEPUT_BITS");
+    return !(e && std::string(e) == "rows");
+  }();
+  return v;
+}
+
 // Must match the carve in hist_bits_kernel (lp_hist_bits.cu).
 size_t smem_bits(int nbits, int kmax, int n, int64_t evt_len, bool smem_evt, int npass, int ng) {
   return a16(16 * (size_t)std::max(nbits, 1)) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
-         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (size_t)npass * n * ng);
+         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (size_t)npass * n * ng) +
+         (bits_gseq() ? a16(4 * (size_t)kmax * 256) : 0);
 }
 
 // Divisor masks of the bits kernel: word (pass, d, g) has bit b set when
@@ -786,7 +796,7 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
     if (g.kind == 5)
-      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, bits_gseq(), g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
@@ -820,7 +830,7 @@ cudaError_t run_hist_stage(const HistPlan& hp, const HistDev& d, cudaStream_t st
     if (g.stage != stage) continue;
     const WorkItem* w = d.work + g.first;
     if (g.kind == 5)
-      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
+      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, bits_gseq(), g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,

@@ -88,10 +88,10 @@ __device__ __forceinline__ void emit(const uint4& inf, uint32_t tm2, uint32_t sj
 // Four blocks per SM fit 64 registers; the widest instantiation needs more
 // (k <= 8 over 128 depths per pass holds 2 x 12 bit planes and 8 slots).
 template <int KMAX, int NG>
-constexpr int bits_min_blocks() { return (KMAX > 4 && NG >= 2) ? 3 : 4; }
+constexpr int bits_min_blocks(bool gseq) { return (!gseq && KMAX > 4 && NG >= 2) ? 3 : 4; }
 
-template <int KMAX, int NG, bool SMEM_EVT>
-__global__ void __launch_bounds__(256, (bits_min_blocks<KMAX, NG>())) hist_bits_kernel(const WorkItem* __restrict__ work,
+template <int KMAX, int NG, bool SMEM_EVT, bool GSEQ>
+__global__ void __launch_bounds__(256, (bits_min_blocks<KMAX, NG>(GSEQ))) hist_bits_kernel(const WorkItem* __restrict__ work,
                                                            const PairDesc* __restrict__ pairs,
                                                            const EntryDesc* __restrict__ entries,
                                                            const DrawConst* __restrict__ draws,
@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(256, (bits_min_blocks<KMAX, NG>())) hist_bits_
   uint32_t* h0 = carve<uint32_t>(p, n);
   uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, (w.evt_len + 1) / 2) : nullptr;
   uint32_t* dm = carve<uint32_t>(p, static_cast<size_t>(npass) * n * NG);
+  uint32_t* scol = GSEQ ? carve<uint32_t>(p, static_cast<size_t>(KMAX) * T) + tid : nullptr;  // sorted slots
 
   const int evt_rel = SMEM_EVT ? w.evt_lo : 0;
   for (int i = tid; i < nbits; i += T) {
@@ -163,6 +164,77 @@ __global__ void __launch_bounds__(256, (bits_min_blocks<KMAX, NG>())) hist_bits_
       for (int j = 1; j < KMAX; ++j)
         if (j < k && s[j] < static_cast<uint32_t>(p1_dmax))
           evt_add<SMEM_EVT>(eb, p1_off + (j - 1) * p1_dmax + static_cast<int>(s[j]));
+    }
+    if (GSEQ) {
+      // group-sequential: one 32-depth group at a time (9 live planes), the
+      // t = 2 events of the whole scenario emitted after the last row from
+      // the row-of-first-collision planes J (one loop per group instead of
+      // one per row and group); t >= 3 events (rare) are emitted per row.
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) scol[j * T] = s[j];
+      for (int ps = 0; ps < npass; ++ps) {
+        const uint32_t* D = dm + static_cast<size_t>(ps) * n * NG;
+        const uint4* I = info + ps * 32 * NG;
+#pragma unroll 1
+        for (int g = 0; g < NG; ++g) {
+          uint32_t M[B], J[3];
+#pragma unroll
+          for (int b = 0; b < B; ++b) M[b] = 0u;
+          J[0] = J[1] = J[2] = 0u;
+#pragma unroll
+          for (int j = 1; j < KMAX; ++j) {
+            if (j >= k) break;
+            const uint32_t sj = s[j];
+            uint32_t R[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) R[b] = 0u;
+#pragma unroll
+            for (int i = 0; i < j; ++i) {
+              const uint32_t m = D[(sj - s[i]) * NG + g];
+              const uint32_t c0 = R[0] & m;
+              R[0] ^= m;
+              if (B == 3) R[2] |= R[1] & c0;
+              R[1] ^= c0;
+            }
+            uint32_t gt, eq;
+            if (B == 3) {
+              gt = R[2] & ~M[2];
+              eq = ~(R[2] ^ M[2]);
+              gt |= eq & R[1] & ~M[1];
+              eq &= ~(R[1] ^ M[1]);
+            } else {
+              gt = R[1] & ~M[1];
+              eq = ~(R[1] ^ M[1]);
+            }
+            gt |= eq & R[0] & ~M[0];
+#pragma unroll
+            for (int b = 0; b < B; ++b) M[b] = (gt & R[b]) | (~gt & M[b]);
+            uint32_t hi = R[1];
+            if (B == 3) hi |= R[2];
+            const uint32_t e2 = gt & ~hi;  // first collision: t = 2 at row j
+            if (j & 1) J[0] |= e2;
+            if (j & 2) J[1] |= e2;
+            if (j & 4) J[2] |= e2;
+            uint32_t e3 = gt & hi;
+            while (e3) {
+              const int b = __ffs(static_cast<int>(e3)) - 1;
+              e3 &= e3 - 1;
+              uint32_t r = ((R[0] >> b) & 1u) | (((R[1] >> b) & 1u) << 1);
+              if (B == 3) r |= ((R[2] >> b) & 1u) << 2;
+              emit<SMEM_EVT>(I[g * 32 + b], r - 1u, sj, eb);
+            }
+          }
+          uint32_t seen = M[0] | M[1];
+          if (B == 3) seen |= M[2];
+          while (seen) {
+            const int b = __ffs(static_cast<int>(seen)) - 1;
+            seen &= seen - 1;
+            const uint32_t jj = ((J[0] >> b) & 1u) | (((J[1] >> b) & 1u) << 1) | (((J[2] >> b) & 1u) << 2);
+            emit<SMEM_EVT>(I[g * 32 + b], 0u, scol[jj * T], eb);
+          }
+        }
+      }
+      continue;
     }
     for (int ps = 0; ps < npass; ++ps) {
       const uint32_t* D = dm + static_cast<size_t>(ps) * n * NG;
@@ -242,29 +314,35 @@ __global__ void __launch_bounds__(256, (bits_min_blocks<KMAX, NG>())) hist_bits_
     }
 }
 
-template <int KMAX, int NG, bool SM>
+template <int KMAX, int NG, bool SM, bool GSEQ>
 static cudaError_t launch_bits_t(int blocks, int threads, size_t smem, cudaStream_t st,
                                  const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
                                  const DrawConst* dr, const uint64_t* binom, const uint32_t* dmask,
                                  uint32_t* evt, uint32_t* h0) {
-  auto fn = hist_bits_kernel<KMAX, NG, SM>;
+  auto fn = hist_bits_kernel<KMAX, NG, SM, GSEQ>;
   cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   fn<<<blocks, threads, smem, st>>>(w, pairs, ents, dr, binom, dmask, evt, h0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_hist_bits(int kmax, int ng, bool smem_evt, int blocks, int threads, size_t smem,
-                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
+cudaError_t launch_hist_bits(int kmax, int ng, bool smem_evt, bool gseq, int blocks, int threads,
+                             size_t smem, cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
                              const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
                              const uint32_t* dmask, uint32_t* evt, uint32_t* h0) {
   if (blocks <= 0) return cudaSuccess;
 #define LP_B(K, G)                                                                                   \
-  if (kmax == K && ng == G)                                                                          \
-    return smem_evt ? launch_bits_t<K, G, true>(blocks, threads, smem, st, w, pairs, ents, dr, binom, \
-                                                dmask, evt, h0)                                      \
-                    : launch_bits_t<K, G, false>(blocks, threads, smem, st, w, pairs, ents, dr,      \
-                                                 binom, dmask, evt, h0);
+  if (kmax == K && ng == G) {                                                                        \
+    if (gseq)                                                                                        \
+      return smem_evt ? launch_bits_t<K, G, true, true>(blocks, threads, smem, st, w, pairs, ents, dr, \
+                                                        binom, dmask, evt, h0)                       \
+                      : launch_bits_t<K, G, false, true>(blocks, threads, smem, st, w, pairs, ents,  \
+                                                         dr, binom, dmask, evt, h0);                 \
+    return smem_evt ? launch_bits_t<K, G, true, false>(blocks, threads, smem, st, w, pairs, ents, dr,  \
+                                                       binom, dmask, evt, h0)                        \
+                    : launch_bits_t<K, G, false, false>(blocks, threads, smem, st, w, pairs, ents, dr, \
+                                                        binom, dmask, evt, h0);                      \
+  }
   LP_B(4, 1)
   LP_B(4, 2)
   LP_B(4, 4)
