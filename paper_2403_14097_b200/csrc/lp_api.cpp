@@ -270,20 +270,10 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
         out[base + n + 1 + out[base + d] + fill[d]++] = (uint16_t)(e - e_lo);
 }
 
-// LIVEPUT_BITS=rows selects the row-parallel variant of the bits kernel (A/B)
-bool bits_gseq() {
-  static const bool v = [] {
-    const char* e = getenv("LIVEPUT_BITS");
-    return !(e && std::string(e) == "rows");
-  }();
-  return v;
-}
-
 // Must match the carve in hist_bits_kernel (lp_hist_bits.cu).
-size_t smem_bits(int nbits, int kmax, int n, int64_t evt_len, bool smem_evt, int npass, int ng) {
-  return a16(16 * (size_t)std::max(nbits, 1)) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
-         (smem_evt ? a16(4 * (size_t)((evt_len + 1) / 2)) : 0) + a16(4 * (size_t)npass * n * ng) +
-         (bits_gseq() ? a16(4 * (size_t)kmax * 256) : 0);
+size_t smem_bits(int nbits, int kmax, int n, int64_t evt_len, bool smem_evt, int ngroups) {
+  return a16(8 * (size_t)std::max(nbits, 1)) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
+         (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(4 * (size_t)ngroups * n) + a16(4 * (size_t)kmax * 256);
 }
 
 // Divisor masks of the bits kernel: word (pass, d, g) has bit b set when
@@ -515,40 +505,43 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       // bit-parallel incidence kernel (lp_hist_bits.cu)
       const int km = pd.k <= 4 ? 4 : 8;
       int e = pd.entry_base;
-      auto shape = [&](int e0, int e1, int64_t ev, bool sm, int* nres_o, int* ng_o, int* np_o) {
+      // groups of 32 resolution depths; a range is a run of entries whose
+      // divisor table, depth info and u32 event cells fit the budget (event
+      // offsets are packed in 20 bits)
+      auto shape = [&](int e0, int e1, int64_t ev, bool sm, int* nres_o, int* ng_o) {
         const int eb0 = (e0 < e1 && hp.entries[e0].P == 1) ? e0 + 1 : e0;
         int nres = 0;
         while (eb0 + nres < e1 && hp.entries[eb0 + nres].tmax >= 2) ++nres;
-        const int ng = nres <= 32 ? 1 : (nres <= 64 ? 2 : 4);
-        const int np = (nres + 32 * ng - 1) / (32 * ng);
+        const int ng = (nres + 31) / 32;
         *nres_o = nres;
         *ng_o = ng;
-        *np_o = np;
-        return smem_bits(np * 32 * ng, km, pd.n, ev, sm, np, ng);
+        return smem_bits(ng * 32, km, pd.n, ev, sm, ng);
       };
       while (e < e_end) {
         int e2 = e;
         int64_t ev = 0;
-        int nres, ng, np;
+        int nres, ng;
         while (e2 < e_end) {
           const EntryDesc& x = hp.entries[e2];
           const int64_t ev2 = ev + (int64_t)std::max(0, x.tmax - 1) * x.Dmax;
-          if (e2 > e && x.tmax >= 2 && shape(e, e2 + 1, ev2, true, &nres, &ng, &np) > kSmemBudgetBits) break;
+          if (e2 > e && x.tmax >= 2 &&
+              (shape(e, e2 + 1, ev2, true, &nres, &ng) > kSmemBudgetBits || ev2 >= (1 << 20)))
+            break;
           ev = ev2;
           ++e2;
         }
-        const size_t sm_need = shape(e, e2, ev, true, &nres, &ng, &np);
+        const size_t sm_need = shape(e, e2, ev, true, &nres, &ng);
         if (nres == 0 && e != pd.entry_base && !(hp.entries[e].P == 1 && hp.entries[e].tmax >= 2)) {
           e = e2;  // nothing to resolve and not the h0 owner
           continue;
         }
         const bool sm = sm_need <= kSmemBudgetBits;
-        const size_t smem = shape(e, e2, ev, sm, &nres, &ng, &np);
+        const size_t smem = shape(e, e2, ev, sm, &nres, &ng);
         const int eb0 = (hp.entries[e].P == 1) ? e + 1 : e;
-        const int doff = build_dmask(hp.entries, eb0, nres, pd.n, ng, np, hp.dmask);
+        const int doff = build_dmask(hp.entries, eb0, nres, pd.n, 1, ng, hp.dmask);
         const int T = 256;
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
-        auto& gv5 = groups[{specs[pi].stage, 5, km * 16 + ng, T, sm ? 1 : 0}];
+        auto& gv5 = groups[{specs[pi].stage, 5, km, T, sm ? 1 : 0}];
         {
           WorkItem w{};
           w.pair = pi;
@@ -559,7 +552,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
           w.evt_len = (int)ev;
           w.smem_evt = sm ? 1 : 0;
           w.dtab_off = doff;
-          w.dtab_len = np;
+          w.dtab_len = ng;
           gv5.push_back({w, pd.t_lo, pd.t_hi, (uint64_t)chunk, smem, 0});
         }
         e = e2;
@@ -796,7 +789,7 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
     if (g.kind == 5)
-      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, bits_gseq(), g.count, g.threads, g.smem, st, w,
+      e = launch_hist_bits(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,
@@ -830,7 +823,7 @@ cudaError_t run_hist_stage(const HistPlan& hp, const HistDev& d, cudaStream_t st
     if (g.stage != stage) continue;
     const WorkItem* w = d.work + g.first;
     if (g.kind == 5)
-      e = launch_hist_bits(g.kmax / 16, g.kmax % 16, g.smem_evt, bits_gseq(), g.count, g.threads, g.smem, st, w,
+      e = launch_hist_bits(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
       e = launch_hist_rows(g.kmax / 16, g.kmax % 16, g.smem_evt, g.count, g.threads, g.smem, st, w,

@@ -27,10 +27,8 @@ cudaError_t launch_hist_inc(int kmax, bool smem_evt, int blocks, int threads, si
                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
                             const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
                             const uint16_t* divtab, uint32_t* evt, uint32_t* h0);
-// gseq: one 32-depth group at a time with the t = 2 events deferred to the
-// end of the scenario (LIVEPUT_BITS=rows: all groups per row, inline events)
-cudaError_t launch_hist_bits(int kmax, int ng, bool smem_evt, bool gseq, int blocks, int threads,
-                             size_t smem, cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
+cudaError_t launch_hist_bits(int kmax, bool smem_evt, int blocks, int threads, size_t smem,
+                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
                              const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
                              const uint32_t* dmask, uint32_t* evt, uint32_t* h0);
 cudaError_t launch_hist_rows(int kreg, int wmax, bool smem_evt, int blocks, int threads,
