@@ -273,7 +273,7 @@ void build_divtab(const std::vector<EntryDesc>& ents, int e_lo, int e_res, int n
 // Must match the carve in hist_bits_kernel (lp_hist_bits.cu).
 size_t smem_bits(int nbits, int kmax, int n, int64_t evt_len, bool smem_evt, int ngroups) {
   return a16(8 * (size_t)std::max(nbits, 1)) + a16(sizeof(DrawConst) * kmax) + a16(4 * (size_t)n) +
-         (smem_evt ? a16(4 * (size_t)evt_len) : 0) + a16(4 * (size_t)ngroups * n) + a16(4 * (size_t)kmax * 256);
+         (smem_evt ? a16(4 * (size_t)(evt_len + 1)) : 0) + a16(4 * (size_t)ngroups * n) + a16(4 * (size_t)kmax * 256);
 }
 
 // Divisor masks of the bits kernel: word (pass, d, g) has bit b set when

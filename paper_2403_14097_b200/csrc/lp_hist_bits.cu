@@ -45,20 +45,16 @@ __device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
 }
 
 // Event of depth info {magic, (evt_off << 12) | Dmax} at slot s_j, level t:
-// cell evt_off + (t - 2) * Dmax + floor(s_j / P), kept only if
-// floor(s_j / P) < Dmax (s_j below lim = P * Dmax).  Shared-memory cells are
-// u32 and the add is predicated, so the loop body has no branch.
+// cell evt_off + (t - 2) * Dmax + floor(s_j / P) when floor(s_j / P) < Dmax
+// (s_j below lim = P * Dmax); otherwise the add goes to the block's spare
+// cell `sink` (never flushed), so the emission loop has no branch.
 template <bool SMEM_EVT>
-__device__ __forceinline__ void emit(uint2 inf, uint32_t tm2, uint32_t sj, uint32_t* eb) {
+__device__ __forceinline__ void emit(uint2 inf, uint32_t tm2, uint32_t sj, uint32_t* eb, uint32_t sink) {
   const uint32_t x = __umulhi(sj, inf.x);
   const uint32_t dmax = inf.y & 0xfffu;
   const uint32_t cell = (inf.y >> 12) + tm2 * dmax + x;
   if (SMEM_EVT) {
-    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(eb)) + 4u * cell;
-    asm volatile(
-        "{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q red.shared.add.u32 [%0], 1;\n\t}" ::"r"(a),
-        "r"(x), "r"(dmax)
-        : "memory");
+    atomicAdd(eb + (x < dmax ? cell : sink), 1u);
   } else if (x < dmax) {
     atomicAdd(eb + cell, 1u);
   }
@@ -96,7 +92,7 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
   uint2* info = carve<uint2>(p, nbits > 0 ? nbits : 1);
   DrawConst* dc = carve<DrawConst>(p, KMAX);
   uint32_t* h0 = carve<uint32_t>(p, n);
-  uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, w.evt_len) : nullptr;
+  uint32_t* evt = SMEM_EVT ? carve<uint32_t>(p, w.evt_len + 1) : nullptr;  // + sink
   uint32_t* dm = carve<uint32_t>(p, static_cast<size_t>(npass) * n * NG);
   uint32_t* scol = carve<uint32_t>(p, static_cast<size_t>(KMAX) * kT) + tid;  // sorted slots
 
@@ -127,6 +123,7 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
   }
   __syncthreads();
   uint32_t* eb = SMEM_EVT ? evt : evt_g + w.evt_lo;
+  const uint32_t sink = static_cast<uint32_t>(w.evt_len);
 
   for (uint64_t t = w.t0 + tid; t < w.t1; t += kT) {
     uint32_t s[KMAX];
@@ -192,7 +189,7 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
             e3 &= e3 - 1;
             uint32_t r = ((R[0] >> b) & 1u) | (((R[1] >> b) & 1u) << 1);
             if (B == 3) r |= ((R[2] >> b) & 1u) << 2;
-            emit<SMEM_EVT>(I[b], r - 1u, sj, eb);
+            emit<SMEM_EVT>(I[b], r - 1u, sj, eb, sink);
           }
         }
         uint32_t seen = M[0] | M[1];
@@ -201,7 +198,7 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
           const int b = __ffs(static_cast<int>(seen)) - 1;
           seen &= seen - 1;
           const uint32_t jj = ((J[0] >> b) & 1u) | (((J[1] >> b) & 1u) << 1) | (((J[2] >> b) & 1u) << 2);
-          emit<SMEM_EVT>(I[b], 0u, scol[jj * kT], eb);
+          emit<SMEM_EVT>(I[b], 0u, scol[jj * kT], eb, sink);
         }
       }
     }
