@@ -41,7 +41,18 @@ constexpr size_t kScnFixedBudget = 64 * 1024;   // entries + event table per blo
 constexpr size_t kSmemBudgetScn = 112 * 1024;   // two blocks per SM
 constexpr size_t kSmemBudgetInc = 75 * 1024;    // three blocks per SM
 constexpr int kIncMaxK = 8;                     // incidence kernel up to k = 8, rows above
-constexpr size_t kSmemBudgetBits = 48 * 1024;   // bits kernel: four 256-thread blocks per SM
+constexpr size_t kSmemBudgetBits8 = 48 * 1024;  // bits kernel, k <= 8: four 256-thread blocks per SM
+constexpr size_t kSmemBudgetBits16 = 64 * 1024; // bits kernel, k <= 16: three blocks per SM
+
+// Largest k resolved by the bits kernel (rows kernel above); LIVEPUT_BITS_MAXK
+// = 8 restores the row kernel for 9 <= k <= 16 (A/B).
+int bits_max_k() {
+  static const int v = [] {
+    const char* e = getenv("LIVEPUT_BITS_MAXK");
+    return e ? std::max(8, std::min(16, atoi(e))) : 16;
+  }();
+  return v;
+}
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -459,7 +470,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     const uint64_t local = pd.t_hi - pd.t_lo;
     if (local == 0 || pd.n_entries == 0) continue;
     const int e_end = pd.entry_base + pd.n_entries;
-    if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512) {
+    if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512 && (bits_off || pd.k > bits_max_k())) {
       // bit-sliced row kernel (lp_hist_rows.cu)
       const RowsShape& rs = rows_shape();
       const int kreg = pd.k <= rs.kreg_max ? 16 : 0;
@@ -501,9 +512,10 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       }
       continue;
     }
-    if (!legacy && pd.k <= kIncMaxK && !bits_off) {
+    if (!legacy && !bits_off && (pd.k <= kIncMaxK || (pd.k <= bits_max_k() && pd.n <= 512))) {
       // bit-parallel incidence kernel (lp_hist_bits.cu)
-      const int km = pd.k <= 4 ? 4 : 8;
+      const int km = pd.k <= 4 ? 4 : (pd.k <= 8 ? 8 : 16);
+      const size_t kSmemBudgetBits = km > 8 ? kSmemBudgetBits16 : kSmemBudgetBits8;
       int e = pd.entry_base;
       // groups of 32 resolution depths; a range is a run of entries whose
       // divisor table, depth info and u32 event cells fit the budget (event

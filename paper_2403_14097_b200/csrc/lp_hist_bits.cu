@@ -62,10 +62,10 @@ __device__ __forceinline__ void emit(uint2 inf, uint32_t tm2, uint32_t sj, uint3
 
 }  // namespace
 
-// KMAX: register scenario size (4 or 8); NG: depth groups per divisor-table
+// KMAX: register scenario size (4, 8 or 16); NG: depth groups per divisor-table
 // word (1: the table is [group][d]).  R and Mx need bits(KMAX - 1) planes.
 template <int KMAX, int NG, bool SMEM_EVT>
-__global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __restrict__ work,
+__global__ void __launch_bounds__(kT, (KMAX > 8 ? 3 : 4)) hist_bits_kernel(const WorkItem* __restrict__ work,
                                                           const PairDesc* __restrict__ pairs,
                                                           const EntryDesc* __restrict__ entries,
                                                           const DrawConst* __restrict__ draws,
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
                                                           const uint32_t* __restrict__ dmask,
                                                           uint32_t* __restrict__ evt_g,
                                                           uint32_t* __restrict__ h0_g) {
-  constexpr int B = KMAX <= 4 ? 2 : 3;
+  constexpr int B = KMAX <= 4 ? 2 : (KMAX <= 8 ? 3 : 4);  // bits of KMAX - 1
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
   const WorkItem w = work[blockIdx.x];
@@ -145,59 +145,62 @@ __global__ void __launch_bounds__(kT, 4) hist_bits_kernel(const WorkItem* __rest
 #pragma unroll 1
       for (int g = 0; g < NG; ++g) {
         const uint2* I = info + (ps * NG + g) * 32;
-        uint32_t M[B], J[3];  // running max of R; row of the first collision
+        uint32_t M[B], J[B];  // running max of R; row of the first collision
 #pragma unroll
-        for (int b = 0; b < B; ++b) M[b] = 0u;
-        J[0] = J[1] = J[2] = 0u;
+        for (int q = 0; q < B; ++q) M[q] = J[q] = 0u;
 #pragma unroll
         for (int j = 1; j < KMAX; ++j) {
           if (j >= k) break;
           const uint32_t sj = s[j];
           uint32_t R[B];
 #pragma unroll
-          for (int b = 0; b < B; ++b) R[b] = 0u;
+          for (int q = 0; q < B; ++q) R[q] = 0u;
 #pragma unroll
           for (int i = 0; i < j; ++i) {  // R += divisor mask of s_j - s_i, bit-sliced
-            const uint32_t m = D[(sj - s[i]) * NG + g];
-            const uint32_t c0 = R[0] & m;
-            R[0] ^= m;
-            if (B == 3) R[2] |= R[1] & c0;
-            R[1] ^= c0;
-          }
-          uint32_t gt, eq;  // gt = R > M, then M = max(M, R)
-          if (B == 3) {
-            gt = R[2] & ~M[2];
-            eq = ~(R[2] ^ M[2]);
-            gt |= eq & R[1] & ~M[1];
-            eq &= ~(R[1] ^ M[1]);
-          } else {
-            gt = R[1] & ~M[1];
-            eq = ~(R[1] ^ M[1]);
-          }
-          gt |= eq & R[0] & ~M[0];
+            uint32_t c = D[(sj - s[i]) * NG + g];
 #pragma unroll
-          for (int b = 0; b < B; ++b) M[b] = (gt & R[b]) | (~gt & M[b]);
-          uint32_t hi = R[1];
-          if (B == 3) hi |= R[2];
+            for (int q = 0; q < B - 1; ++q) {
+              const uint32_t nc = R[q] & c;
+              R[q] ^= c;
+              c = nc;
+            }
+            R[B - 1] |= c;  // R <= j <= KMAX - 1 never overflows B bits
+          }
+          // gt = R > M (per bit, most significant plane first), M = max(M, R)
+          uint32_t gt = 0u, eq = ~0u;
+#pragma unroll
+          for (int q = B - 1; q >= 0; --q) {
+            gt |= eq & R[q] & ~M[q];
+            eq &= ~(R[q] ^ M[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < B; ++q) M[q] = (gt & R[q]) | (~gt & M[q]);
+          uint32_t hi = 0u;
+#pragma unroll
+          for (int q = 1; q < B; ++q) hi |= R[q];
           const uint32_t e2 = gt & ~hi;  // first collision: t = 2 at row j
-          if (j & 1) J[0] |= e2;
-          if (j & 2) J[1] |= e2;
-          if (j & 4) J[2] |= e2;
+#pragma unroll
+          for (int q = 0; q < B; ++q)
+            if ((j >> q) & 1) J[q] |= e2;
           uint32_t e3 = gt & hi;  // t = R + 1 >= 3
           while (e3) {
             const int b = __ffs(static_cast<int>(e3)) - 1;
             e3 &= e3 - 1;
-            uint32_t r = ((R[0] >> b) & 1u) | (((R[1] >> b) & 1u) << 1);
-            if (B == 3) r |= ((R[2] >> b) & 1u) << 2;
+            uint32_t r = 0u;
+#pragma unroll
+            for (int q = 0; q < B; ++q) r |= ((R[q] >> b) & 1u) << q;
             emit<SMEM_EVT>(I[b], r - 1u, sj, eb, sink);
           }
         }
-        uint32_t seen = M[0] | M[1];
-        if (B == 3) seen |= M[2];
+        uint32_t seen = 0u;
+#pragma unroll
+        for (int q = 0; q < B; ++q) seen |= M[q];
         while (seen) {
           const int b = __ffs(static_cast<int>(seen)) - 1;
           seen &= seen - 1;
-          const uint32_t jj = ((J[0] >> b) & 1u) | (((J[1] >> b) & 1u) << 1) | (((J[2] >> b) & 1u) << 2);
+          uint32_t jj = 0u;
+#pragma unroll
+          for (int q = 0; q < B; ++q) jj |= ((J[q] >> b) & 1u) << q;
           emit<SMEM_EVT>(I[b], 0u, scol[jj * kT], eb, sink);
         }
       }
@@ -238,6 +241,7 @@ cudaError_t launch_hist_bits(int kmax, bool smem_evt, int blocks, int threads, s
                                                  dmask, evt, h0);
   LP_B(4)
   LP_B(8)
+  LP_B(16)
 #undef LP_B
   return cudaErrorInvalidValue;
 }

@@ -56,7 +56,7 @@ def test_execution_modes_agree():
                 {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"},
                 {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"},
                 {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
-                {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"}, {"LIVEPUT_HIST_KERNEL": "inc"},
+                {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"}, {"LIVEPUT_HIST_KERNEL": "inc"}, {"LIVEPUT_BITS_MAXK": "8"},
                 {"LIVEPUT_HIST_KERNEL": "norows"}, {"LIVEPUT_ROWS_SHAPE": "160,56,8"},
                 {"LIVEPUT_ROWS_SHAPE": "96,40,2"}, {"LIVEPUT_ROWS_KREG": "0"}):
         assert _run(env) == base, env
