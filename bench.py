@@ -33,6 +33,11 @@ EXTENSION = [24, 21, 21, 19, 22, 20, 20, 17, 18, 18, 16, 19]
 PROFILE = "lm_1p5b"
 
 
+# forecast-like availability (tools/prof_replan.py PREDICT): drops k <= 8, the
+# regime the Proactive policy produces (predictor.cpp:228-232 clamps to 8)
+PREDICT_NSEQ = [256, 250, 252, 245, 245, 248, 240, 236, 238, 232, 232, 229, 226]
+
+
 def north_star_nseq(n_instances: int = 256, lookahead: int = 24):
     """SURVEY.md §8c known-answer availability pattern (I=12) extended to I=24,
     scaled from 32 to n_instances (drops of up to 5*N/32 instances)."""
@@ -177,6 +182,42 @@ class RefArm:
                 f"instead of the workload's trial count, {self.threads} threads")
 
 
+def load_profile_issue():
+    """Issue-slot utilisation of the dominant kernel from the committed ncu
+    capture (sm__inst_issued / (SM cycles x 4 schedulers))."""
+    p = ROOT / "profiles" / "issue.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def reference_1thread_replan(w, current, n_seq, trials, pilot=(1000, 2000)):
+    """BASELINE.md §4.2: the reference's Planner::dp_optimize, cold (fresh
+    Planner), one thread, on the same inputs — timed at two reduced trial
+    counts and extrapolated linearly in trials (t = a + b*T) to the
+    workload's count (the histogram is >= 95% of the time and linear in T)."""
+    import ctypes as C
+    from oracle.oracle import ref_lib
+    from paper_2403_14097_b200.model import CostTable, PlannerOptions
+    L = ref_lib()
+    prof, keep = w.to_c()
+    costs = CostTable().to_c()
+    ns = (C.c_int * len(n_seq))(*n_seq)
+    cd, cp = (current.pipelines, current.stages) if current else (0, 0)
+    secs = []
+    for t in pilot:
+        o = PlannerOptions(mc_trials=t).to_c()
+        secs.append(L.ref_bench_replan(C.byref(prof), C.byref(costs), C.byref(o), cd, cp, ns, len(n_seq)))
+    b = (secs[1] - secs[0]) / (pilot[1] - pilot[0])
+    a = secs[0] - b * pilot[0]
+    return {"reference_1thread_dp_optimize_s": a + b * trials,
+            "reference_1thread_fit": {"trials": list(pilot), "seconds": secs, "extrapolated_to": trials,
+                                      "how": "cold Planner::dp_optimize, 1 thread, same inputs; t = a + b*trials"}}
+
+
 def cpu_reference_sample(n_seq, target_s=6.0):
     arm = RefArm(n_seq).calibrate(target_s / 3)
     tot_r, tot_s = 0, 0.0
@@ -191,7 +232,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    n_seq = north_star_nseq(args.instances, args.lookahead)
+    n_seq = workload_nseq(args)
     steps, warm = args.steps, args.warmup
     try:
         from oracle.oracle import REF_LIB
@@ -220,10 +261,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def workload_nseq(args):
+    if args.workload == "predict":
+        return list(PREDICT_NSEQ)
+    if args.workload == "ns12":
+        return north_star_nseq(args.instances, 12)
+    return north_star_nseq(args.instances, args.lookahead)
+
+
 def workload_config(args, n_seq):
-    return {"workload": f"BASELINE configs[3]: N={args.instances} instances, {args.lookahead}-interval lookahead, "
-                        f"{args.trials:.0e} samples/point, GPT-2 1.5B (D,P) table, controlled n_seq",
-            "instances": args.instances, "lookahead": args.lookahead, "mc_trials": args.trials,
+    name = {"bench": f"BASELINE configs[3]: N={args.instances} instances, {args.lookahead}-interval lookahead, "
+                     f"{args.trials:.0e} samples/point, GPT-2 1.5B (D,P) table, controlled n_seq",
+            "ns12": f"north-star re-plan: N={args.instances}, 12-interval lookahead, {args.trials:.0e} samples/point, "
+                    "GPT-2 1.5B (D,P) table, controlled n_seq",
+            "predict": f"forecast-like re-plan: N=256, 12-interval lookahead, {args.trials:.0e} samples/point, "
+                       "GPT-2 1.5B (D,P) table, drops k <= 8 (Proactive regime)"}[args.workload]
+    return {"workload": name,
+            "instances": n_seq[0], "lookahead": len(n_seq) - 1, "mc_trials": args.trials,
             "profile": PROFILE, "n_seq": n_seq, "mc_pairs": sum(1 for p in distinct_pairs(n_seq) if p[1] > 0),
             "l2": "flushed (256 MiB write) between timed steps",
             "parallelism": f"trial-sharded x{args.gpus} + ncclAllReduce(u32 histograms)"}
@@ -240,6 +294,9 @@ def main():
     ap.add_argument("--trials", type=int, default=1_000_000)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="bench", choices=["bench", "ns12", "predict"],
+                    help="bench: BASELINE configs[3] (default); ns12: the north-star I=12 re-plan; "
+                         "predict: forecast-like drops k <= 8")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -255,9 +312,9 @@ def main():
     from paper_2403_14097_b200.planner import Planner, nccl_unique_id, reactive_plan
 
     w = PROFILES[PROFILE]()
-    n_seq = north_star_nseq(args.instances, args.lookahead)
+    n_seq = workload_nseq(args)
     current = reactive_plan(n_seq[0], w)
-    opt = PlannerOptions(mc_trials=args.trials, lookahead=args.lookahead)
+    opt = PlannerOptions(mc_trials=args.trials, lookahead=len(n_seq) - 1)
     pl = Planner(w, CostTable(), opt, device=local)
     if world > 1:
         import torch.distributed as dist
@@ -328,6 +385,28 @@ def main():
     e2e_value = resolutions * args.steps / e2e_s
     assert [s.config for s in plan_e2e] == [s.config for s in plan_dev]
 
+    # ---- the north-star re-plan (N=256, I=12, 1e6): device and end-to-end ---
+    ns_ms = None
+    if args.workload == "bench" and args.trials == 1_000_000 and args.instances == 256:
+        ns = north_star_nseq(256, 12)
+        cur12 = reactive_plan(ns[0], w)
+        pl.prepare(cur12, ns)
+        dev12 = []
+        for _ in range(3 + args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            pl.execute()
+            dev12.append(pl.stats().total_ms)
+        barrier()
+        t_e = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            pl.dp_optimize(cur12, ns)
+            t_e.append(time.perf_counter() - t0)
+        ns_ms = {"device_ms": max_over_ranks(statistics.median(dev12[3:])),
+                 "e2e_ms": max_over_ranks(1e3 * statistics.median(t_e)),
+                 "target_ms": 100.0, "n_seq": ns}
+
     if rank != 0:
         pl.close()
         if world > 1:
@@ -341,7 +420,9 @@ def main():
     peak_gops = n_sm * 4 * 32 * sm_mhz * 1e6 / 1e9
     hist_med = statistics.median(hist_ms)
     achieved_gops = st.hist_alg_ops / (hist_med / 1e3) / 1e9
+    survey_gops = st.hist_survey_ops / (hist_med / 1e3) / 1e9
     traffic = load_profile_traffic()
+    issue = load_profile_issue()
     line = {
         "metric": "liveput scenarios/sec", "value": value, "unit": "resolutions/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -351,12 +432,22 @@ def main():
         "replan_ms": ms_per_step,
         "phase_ms": {"histograms": hist_med, "allreduce": statistics.median(red_ms), "dp": statistics.median(dp_ms)},
         "resolutions_per_step": resolutions, "scenarios_per_step": st.scenarios,
+        "scenarios_per_s": st.scenarios * args.steps / (dev_ms / 1e3),
         "plan": [[s.config.pipelines, s.config.stages] if s.config else None for s in plan_dev],
+        "plan_step_hex": [[s.expected_committed.hex(), s.expected_mig_cost_s.hex()] for s in plan_dev],
+        "northstar_i12": ns_ms,
         "gpu_launches": st.kernel_launches * args.steps,
         "e2e": {"value": e2e_value, "unit": "resolutions/s", "ms_per_step": e2e_s * 1e3 / args.steps,
                 "h2d_bytes_per_step": int(st2.h2d_bytes), "d2h_bytes_per_step": int(st2.d2h_bytes)},
         "roofline": {"bound": "int-issue", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
-                     "frac": achieved_gops / peak_gops,
+                     "frac": achieved_gops / peak_gops, "frac_model": achieved_gops / peak_gops,
+                     "model": "int32 ops of the algorithms as run (DESIGN.md §5.2): generation 20+35k per "
+                              "scenario; bits kernel k(k-1)/2 x (2B+1) + (k-1) x (5B+3) per 32-depth group; "
+                              "row kernel Dmax x ceil(P/32) x (3B+4) per depth; events not counted",
+                     "frac_survey_model": survey_gops / peak_gops,
+                     "survey_ops_per_step": st.hist_survey_ops,
+                     "issue_frac": issue.get("issue_frac") if issue else None,
+                     "issue_source": issue.get("source") if issue else None,
                      "peak_source": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz measured SM clock "
                                     "(1 int32 lane-op/lane/cycle issue)",
                      "kernel": "hist_* (K1: scenario generation + threshold-event resolution), incl. finalize",
@@ -369,6 +460,7 @@ def main():
             v, arm = cpu_reference_sample(n_seq, target_s=args.ref_seconds)
             line["cpu_baseline"] = {"value": v, "unit": "resolutions/s", "cores": arm.threads, "kind": "reference",
                                     "sample": "reference Planner::survivor_histogram over " + arm.info()}
+            line["cpu_baseline"].update(reference_1thread_replan(w, current, n_seq, args.trials))
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line), flush=True)

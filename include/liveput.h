@@ -114,11 +114,16 @@ typedef struct {
   double reduce_ms;          /* device time of the cross-rank histogram reduce */
   double dp_ms;              /* device time of the DP kernels */
   double total_ms;           /* device time of the whole execute */
-  uint64_t hist_alg_ops;     /* algorithmic int32-equivalent ops of the histogram kernel */
+  uint64_t hist_alg_ops;     /* int32-equivalent ops of the resolution algorithms as run:
+                                scenario generation 20 + 35k, the bits kernel's slot-pair
+                                lookups / bit-sliced adds / row compares, the row kernel's
+                                Dmax x ceil(P/32) x (3B+4) per depth */
   uint64_t h2d_bytes;        /* bytes copied host->device by the last prepare */
   uint64_t d2h_bytes;        /* bytes copied device->host by the last fetch */
   double prepare_ms;         /* host wall time of the last lp_prepare (tables + H2D issue) */
   uint64_t cached_pairs;     /* (n, k) ensembles served from the histogram cache */
+  uint64_t hist_survey_ops;  /* SURVEY.md §8d's reference-equivalent model: per scenario
+                                S(k) = 20 + 35k plus R(k) = 6k per depth */
 } lp_stats;
 
 typedef struct lp_handle lp_handle;

@@ -96,6 +96,7 @@ class lp_stats(C.Structure):
         ("d2h_bytes", C.c_uint64),
         ("prepare_ms", C.c_double),
         ("cached_pairs", C.c_uint64),
+        ("hist_survey_ops", C.c_uint64),
     ]
 
 

@@ -234,6 +234,7 @@ struct HistPlan {
   std::vector<Stage> stages;
   int64_t evt_len = 0, h0_len = 0, hist_len = 0;
   uint64_t scenarios = 0, local_scenarios = 0, resolutions = 0, alg_ops = 0;
+  uint64_t model_ops = 0;  // int ops of the algorithms actually run (op_model_*)
   int mc_pairs = 0, exact_pairs = 0;
 };
 
@@ -331,6 +332,25 @@ size_t smem_scn(int ne_res, int k, int n, int64_t evt_len, bool smem_evt, int T,
 // R(k) = 6k per (scenario, depth); no per-(scenario, config) term.
 uint64_t alg_ops(uint64_t scen, int k, int depths) {
   return scen * (20ull + 35ull * k + 6ull * k * (uint64_t)depths);
+}
+
+// Int32-equivalent ops per scenario of the resolution algorithms as run
+// (the "model" roofline).  Event emission is not counted.
+int planes_of(int v) {  // bits needed for 0..v
+  int b = 1;
+  while ((1 << b) <= v) ++b;
+  return b;
+}
+// bits kernel, per 32-depth group: k(k-1)/2 slot pairs x (table lookup 2 +
+// bit-sliced add 2B-1) and k-1 rows x (compare 3B + max B + J/event masks B+3)
+uint64_t op_model_bits(int k, int km, int groups) {
+  const uint64_t B = planes_of(km - 1), kp = (uint64_t)k * (k - 1) / 2;
+  return (uint64_t)groups * (kp * (2 * B + 1) + (uint64_t)std::max(k - 1, 0) * (5 * B + 3));
+}
+// row kernel, per depth: Dmax rows x ceil(P/32) words x (3B + 4), B = bits(tmax)
+uint64_t op_model_rows(const EntryDesc& e) {
+  if (e.tmax < 2) return 0;
+  return (uint64_t)e.Dmax * ((e.P + 31) / 32) * (3ull * planes_of(e.tmax) + 4ull);
 }
 
 // Rng::below(b) constants (rng.hpp:23-30) for b = 1 .. kMaxN, computed once
@@ -438,6 +458,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     hp.local_scenarios += local;
     hp.resolutions += sp.count * sp.ref_keys;
     hp.alg_ops += alg_ops(local, k, pd.n_entries);
+    hp.model_ops += local * (20ull + 35ull * k);  // scenario generation, once per scenario
   }
 
   mark("pairs");
@@ -495,6 +516,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact) > rs.smem)
           T -= 32;
         const size_t smem = smem_rows(e_res - e, pd.k, pd.n, ev, sm, T, kreg, pd.exact);
+        for (int q = e; q < e_res; ++q) hp.model_ops += local * op_model_rows(hp.entries[q]);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         auto& gv1 = groups[{specs[pi].stage, 4, kreg * 16 + wmax, T, sm ? 1 : 0}];
         {
@@ -551,6 +573,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         const size_t smem = shape(e, e2, ev, sm, &nres, &ng);
         const int eb0 = (hp.entries[e].P == 1) ? e + 1 : e;
         const int doff = build_dmask(hp.entries, eb0, nres, pd.n, 1, ng, hp.dmask);
+        hp.model_ops += local * op_model_bits(pd.k, km, ng);
         const int T = 256;
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
         auto& gv5 = groups[{specs[pi].stage, 5, km, T, sm ? 1 : 0}];
@@ -590,6 +613,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (e_res < e2 && hp.entries[e_res].tmax >= 2) ++e_res;
         const int doff = (int)hp.divtab.size();
         build_divtab(hp.entries, e, e_res, pd.n, hp.divtab);
+        hp.model_ops += local * 6ull * pd.k * (uint64_t)(e_res - e);
         const int dlen = (int)hp.divtab.size() - doff;
         const bool sm = a16(sizeof(EntryDesc) * (e2 - e)) + a16(4 * (size_t)ev) <= kScnFixedBudget;
         int T = 128;
@@ -642,6 +666,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
         while (T > 32 && smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw) > kSmemBudgetScn) T >>= 1;
         const size_t smem = smem_scn(e_res - e, pd.k, pd.n, ev, sm, T, uw);
         const uint64_t chunk = std::min<uint64_t>((uint64_t)T * 16, per_block);
+        hp.model_ops += local * 6ull * pd.k * (uint64_t)(e_res - e);
         auto& gv3 = groups[{specs[pi].stage, 2, kreg, T, sm ? 1 : 0}];
         {
           WorkItem w{};
@@ -1641,7 +1666,8 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->stats.mc_pairs = h->hp.mc_pairs;
   h->stats.exact_pairs = h->hp.exact_pairs;
   h->stats.horizon = H;
-  h->stats.hist_alg_ops = h->hp.alg_ops;
+  h->stats.hist_alg_ops = h->hp.model_ops;
+  h->stats.hist_survey_ops = h->hp.alg_ops;
   h->stats.cached_pairs = specs.size() - fresh.size();
   auto& ps = h->ps;
   ps.len = len;
