@@ -73,6 +73,15 @@ __device__ __forceinline__ double transition_cost(int m, int sd, int sp, int td,
 // throughput(D, P).
 // Bin accessors: probability of bin d, and eight bins d0, d0-1, ... d0-7
 // (0.0 below d = 0) fetched together.
+// Eight bins that are all +0.0 (probabilities are never -0.0) add nothing:
+// adding +0.0 to a non-negative sum is exact, so a zero chunk is skipped.
+__device__ __forceinline__ bool zero8(const double (&pr)[8]) {
+  unsigned long long o = 0ull;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) o |= static_cast<unsigned long long>(__double_as_longlong(pr[u]));
+  return o == 0ull;
+}
+
 struct ProbPtr {
   const double* hp;
   __device__ __forceinline__ double operator()(int d) const { return hp[d]; }
@@ -147,6 +156,7 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     for (int d0 = d; d0 >= 0; d0 -= 8) {
       double pr[8];
       prob.chunk(d0, pr);
+      if (zero8(pr)) continue;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr[u], rate), teff_pipe));
@@ -166,6 +176,7 @@ __device__ __forceinline__ PhiOut phi_dev(const NodeCfg& pv, const NodeCfg& nx, 
     for (int d0 = dmax; d0 >= 0; d0 -= 8) {
       double pr[8];
       prob.chunk(d0, pr);
+      if (zero8(pr)) continue;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int m = sd - (d0 - u);  // bins past d = 0 carry p = 0
@@ -255,6 +266,7 @@ __device__ __forceinline__ void phi_fast2(const NodeCfg& a, const NodeCfg& b, co
       pa[u] = (i0 + u <= da) ? qa[-u] : 0.0;
       pb[u] = (i0 + u <= db) ? qb[-u] : 0.0;
     }
+    if (zero8(pa) && zero8(pb)) continue;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       ca = __dadd_rn(ca, __dmul_rn(__dmul_rn(pa[u], rate), K.teff_pipe));
