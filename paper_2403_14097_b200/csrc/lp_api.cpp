@@ -953,6 +953,7 @@ struct lp_handle {
   cudaEvent_t ev_hist[kMaxStages] = {};       // ... done
   cudaEvent_t ev_start = nullptr;             // scratch cleared for this execute
   cudaEvent_t ev_join = nullptr;
+  std::vector<cudaEvent_t> tl_ev;  // LIVEPUT_TIMELINE: one event per DP level (diagnostics)
   std::vector<int> level_need;  // per DP level: the last stage it must wait for (-1: none)
   std::string err;
   ncclComm_t comm = nullptr;
@@ -1279,6 +1280,7 @@ void lp_destroy(lp_handle* h) {
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : h->ev_hist)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->tl_ev) cudaEventDestroy(ev);
   for (auto& sh : h->stream_hist)
     if (sh) {
       cudaStreamSynchronize(sh);
@@ -1860,6 +1862,14 @@ lp_status exec_hist(lp_handle* h) {
 // j waits only for the stage holding the histograms it reads, so the DP of
 // the early intervals overlaps the sampling of the later ones; the DP
 // stream is joined back into the handle's stream at the end.
+// LIVEPUT_TIMELINE=1: lp_get_stats prints, relative to the start of the
+// execute, when each stage's histogram kernels and normalisation finished
+// and when each DP level finished (per-level launches only).
+bool timeline() {
+  static const bool on = getenv("LIVEPUT_TIMELINE") != nullptr;
+  return on;
+}
+
 lp_status exec_dp(lp_handle* h) {
   cudaStream_t st = h->stream_dp;
   int launches = 0;
@@ -1930,6 +1940,14 @@ lp_status exec_dp(lp_handle* h) {
       LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, pdl, st, lv, cfg, pcost,
                                 histp, thr, throw_, h->S, val, mig, par, stc, stm));
       ++launches;
+      if (timeline()) {
+        while ((int)h->tl_ev.size() <= j) {
+          cudaEvent_t e;
+          LP_CUDA(h, cudaEventCreate(&e));
+          h->tl_ev.push_back(e);
+        }
+        LP_CUDA(h, cudaEventRecord(h->tl_ev[j], st));
+      }
     }
     LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
                                dptr<lp_plan_step>(h->work, h->w_plan),
@@ -2204,6 +2222,20 @@ lp_status lp_get_stats(const lp_handle* hc, lp_stats* out) {
     h->stats.reduce_ms = b;
     h->stats.dp_ms = c;
     h->stats.total_ms = (double)a + b + c;
+    if (timeline()) {
+      auto rel = [&](cudaEvent_t e) {
+        float t = -1.f;
+        cudaEventElapsedTime(&t, h->ev[0], e);
+        return t;
+      };
+      const int nst = (int)h->hp.stages.size();
+      fprintf(stderr, "[timeline] rank %d:", h->rank);
+      for (int q = 0; q < nst && nst > 1; ++q)
+        fprintf(stderr, " s%d hist %.3f norm %.3f |", q, rel(h->ev_hist[q]), rel(h->ev_stage[q]));
+      for (int j = 0; j < (int)h->tl_ev.size() && j < h->horizon; ++j)
+        fprintf(stderr, " L%d(%d) %.3f", j, j < (int)h->level_need.size() ? h->level_need[j] : -1, rel(h->tl_ev[j]));
+      fprintf(stderr, " | end %.3f\n", rel(h->ev[3]));
+    }
   }
   *out = h->stats;
   return LP_OK;
