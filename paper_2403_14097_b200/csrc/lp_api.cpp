@@ -56,6 +56,14 @@ int bits_max_k() {
 
 size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
+// LIVEPUT_TIMELINE=1: lp_get_stats prints, relative to the start of the
+// execute, when each stage's histogram kernels and normalisation finished
+// and when each DP level finished (per-level launches only).
+bool timeline() {
+  static const bool on = getenv("LIVEPUT_TIMELINE") != nullptr;
+  return on;
+}
+
 // Row-kernel block shape: threads per block cap, shared-memory budget per
 // block and the entries + event-table share of it. LIVEPUT_ROWS_SHAPE =
 // "T,smem_kb,fixed_kb" overrides the defaults (256, 112, 64) for A/B runs.
@@ -1242,17 +1250,28 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
   h->opt = *options;
   h->cs = cost_scalars(*costs);
   h->device = device;
+  // LIVEPUT_PRIO=1: DP and library streams at the highest priority, stage s
+  // histogram streams one step lower each (A/B of the stage pipelining)
+  static const bool prio = [] {
+    const char* pe = getenv("LIVEPUT_PRIO");
+    return pe && pe[0] == '1';
+  }();
+  int least = 0, greatest = 0;
+  if (prio) cudaDeviceGetStreamPriorityRange(&least, &greatest);
   if ((e = cudaSetDevice(device)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&h->stream_dp, cudaStreamNonBlocking)) != cudaSuccess) {
+      (e = cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, greatest)) != cudaSuccess ||
+      (e = cudaStreamCreateWithPriority(&h->stream_dp, cudaStreamNonBlocking, greatest)) != cudaSuccess) {
     delete h;
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }
+  const unsigned tflag = timeline() ? cudaEventDefault : cudaEventDisableTiming;
   for (auto& ev : h->ev) cudaEventCreate(&ev);
   for (auto& ev : h->ev_up) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  for (auto& ev : h->ev_stage) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  for (auto& ev : h->ev_hist) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  for (auto& sh : h->stream_hist) cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking);
+  for (auto& ev : h->ev_stage) cudaEventCreateWithFlags(&ev, tflag);
+  for (auto& ev : h->ev_hist) cudaEventCreateWithFlags(&ev, tflag);
+  for (int q = 0; q < lp_handle::kMaxStages; ++q)
+    cudaStreamCreateWithPriority(&h->stream_hist[q], cudaStreamNonBlocking,
+                                 prio ? std::min(least, greatest + 1 + q) : 0);
   cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
   {
@@ -1862,13 +1881,6 @@ lp_status exec_hist(lp_handle* h) {
 // j waits only for the stage holding the histograms it reads, so the DP of
 // the early intervals overlaps the sampling of the later ones; the DP
 // stream is joined back into the handle's stream at the end.
-// LIVEPUT_TIMELINE=1: lp_get_stats prints, relative to the start of the
-// execute, when each stage's histogram kernels and normalisation finished
-// and when each DP level finished (per-level launches only).
-bool timeline() {
-  static const bool on = getenv("LIVEPUT_TIMELINE") != nullptr;
-  return on;
-}
 
 lp_status exec_dp(lp_handle* h) {
   cudaStream_t st = h->stream_dp;
