@@ -430,8 +430,16 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       max_dm = std::max(max_dm, Dm);
       hp.entries.push_back(e);
     }
-    if (pd.variant == 1 && k > kMaxK && max_dm > kMaxK) {
-      err = "liveput: n_minus > 255 with more than 255 pipelines per depth is not supported";
+    // only the first-generation counter kernel (LIVEPUT_HIST_KERNEL=legacy)
+    // keeps u8 class counts; the row (B <= 10 planes) and scenario-major
+    // (12-bit counts) kernels resolve any k
+    static const bool legacy_env = [] {
+      const char* e = getenv("LIVEPUT_HIST_KERNEL");
+      return e && std::string(e) == "legacy";
+    }();
+    if (legacy_env && pd.variant == 1 && k > kMaxK && max_dm > kMaxK) {
+      err = "liveput: n_minus > 255 with more than 255 pipelines per depth needs the default kernels "
+            "(LIVEPUT_HIST_KERNEL=legacy keeps u8 counters)";
       return LP_EUNSUPPORTED;
     }
     if (sp.exact) {

@@ -330,8 +330,8 @@ __device__ __forceinline__ void walk_gen(const uint32_t* BMc, int T, uint32_t P,
 //   2..4    Dmax <= 4: walk_small
 //   5, 6    slot walk (ELEMS: k <= 16 slots in registers; P <= 16 and 10..64
 //           rows), rise mask u32 / u64
-//   8 + B   walk_rows (walk_rows1 with a u64 rise mask when W = 1, Dmax <= 64)
-//   16 + B  walk_rows1 with a u32 rise mask (W = 1, Dmax <= 32)
+//   8 + B   walk_rows (walk_rows1 with a u64 rise mask when W = 1, Dmax <= 64), B <= 10
+//   24 + B  walk_rows1 with a u32 rise mask (W = 1, Dmax <= 32)
 // B = plane count = bits(tmax).
 template <bool ELEMS>
 __device__ __forceinline__ int depth_class(const EntryDesc& e) {
@@ -340,7 +340,7 @@ __device__ __forceinline__ int depth_class(const EntryDesc& e) {
   if (e.Dmax == 2) return (1 << 5) | 7;  // all two-row depths: dm2_run
   if (e.Dmax <= 4) return (W << 5) | e.Dmax;
   const int B = 32 - __clz(static_cast<uint32_t>(e.tmax));
-  return (W << 5) | ((W == 1 && e.Dmax <= 32 ? 16 : 8) + B);
+  return (W << 5) | ((W == 1 && e.Dmax <= 32 ? 24 : 8) + B);  // B <= 10 (tmax <= n <= 512)
 }
 
 template <int KS, bool SMEM_EVT, typename M>
@@ -379,13 +379,13 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
   if (W == 1 && KS > 1 && mode == 5) return elems_run<KS, SMEM_EVT, uint32_t>(ents, e0, e1, eb, sl);
   if (W == 1 && KS > 1 && mode == 6)
     return elems_run<KS, SMEM_EVT, unsigned long long>(ents, e0, e1, eb, sl);
-  if (W == 1 && mode > 16) {
+  if (W == 1 && mode > 24) {
     switch (mode) {
-      case 18: LP_R1(2)
-      case 19: LP_R1(3)
-      case 20: LP_R1(4)
-      case 21: LP_R1(5)
-      case 22: LP_R1(6)
+      case 26: LP_R1(2)
+      case 27: LP_R1(3)
+      case 28: LP_R1(4)
+      case 29: LP_R1(5)
+      case 30: LP_R1(6)
       default: break;  // tmax <= Dmax <= 32: at most 6 planes
     }
   }
@@ -399,7 +399,10 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
     case 13: LP_RUN((walk_gen<W, 5, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
     case 14: LP_RUN((walk_gen<W, 6, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
     case 15: LP_RUN((walk_gen<W, 7, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
-    default: LP_RUN((walk_gen<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    case 16: LP_RUN((walk_gen<W, 8, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    // k > 255 with more than 255 rows: only depths 1 and 2 at n <= 512
+    case 17: LP_RUN((walk_gen<(W < 2 ? W : 1), 9, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
+    default: LP_RUN((walk_gen<(W < 2 ? W : 1), 10, SMEM_EVT>(BMc, T, P, Dm, eb, eo)))
   }
 #undef LP_R1
 #undef LP_RUN

@@ -17,7 +17,8 @@
 //   * depths with Dmax <= kComb count class members with a "comb" of bitmap
 //     tests c_j = 1 + sum_{y=1..q_j} BM[s_j - y*P] (no per-class state);
 //   * the other (small) depths count classes in stamped u16 counters,
-//     (stamp << 8) | count, so nothing is cleared between scenarios.
+//     (stamp << 8) | count (12-bit counts when k > 255), so nothing is
+//     cleared between scenarios.
 //
 // Events (t >= 2) go to a per-block shared-memory table with RED.ADD and are
 // flushed to HBM once per block; t = 1 events are the per-scenario minimum
@@ -98,7 +99,10 @@ __global__ void __launch_bounds__(256, 2) hist_scn_kernel(const WorkItem* __rest
   uint32_t* BMc = BM + tid;
   uint32_t* Uc = U + tid;
   unsigned char* ctr = reinterpret_cast<unsigned char*>(U) + 4 * tid;  // u16 counters, swizzled
-  uint32_t stamp = 256;  // forces a clear before first use
+  // (stamp << cb) | count: 8-bit counts, or 12-bit when a class can hold
+  // more than 255 slots (k > 255; Dmax <= n / 2 <= 1024 then)
+  const uint32_t cb = k > 255 ? 12u : 8u, cmask = (1u << cb) - 1u, smax = (1u << (16u - cb)) - 1u;
+  uint32_t stamp = smax + 1u;  // forces a clear before first use
 
   for (uint64_t t = w.t0 + tid; t < w.t1; t += T) {
     // ---- draw scenario t: sorted slots into Sc[j*T], bitmap into BMc[w*T]
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(256, 2) hist_scn_kernel(const WorkItem* __rest
       }
     } else {
       gen_mc_generic(pd.seed, t, n, k, dc, Uc, T, BMc, T, Sc, T);
-      stamp = 256;  // the map overwrote the counters
+      stamp = smax + 1u;  // the map overwrote the counters
     }
     if (own_h0 && k > 0) atomicAdd(&h0[Sc[0]], 1u);
 
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(256, 2) hist_scn_kernel(const WorkItem* __rest
           }
         }
       } else {
-        if (++stamp > 255u) {
+        if (++stamp > smax) {
           for (int i = 0; i < uw; ++i) Uc[i * T] = 0u;
           stamp = 1;
         }
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(256, 2) hist_scn_kernel(const WorkItem* __rest
           const uint32_t r = sv - q * P;
           uint16_t* a = reinterpret_cast<uint16_t*>(ctr + ((r >> 1) * T << 2) + ((r & 1) << 1));
           const uint32_t h = *a;
-          const uint32_t c = ((h >> 8) == stamp) ? (h & 0xffu) + 1u : 1u;
-          *a = static_cast<uint16_t>((stamp << 8) | c);
+          const uint32_t c = ((h >> cb) == stamp) ? (h & cmask) + 1u : 1u;
+          *a = static_cast<uint16_t>((stamp << cb) | c);
           if (static_cast<int>(c) > mx) {
             mx = static_cast<int>(c);
             evt_add<SMEM_EVT>(eb + (mx - 2) * Dm + static_cast<int>(q));

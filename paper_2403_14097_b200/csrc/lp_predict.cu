@@ -24,8 +24,35 @@ std::string& global_error();  // lp_api.cpp
 
 namespace {
 
-constexpr int kMaxHist = 64;    // history_len supported
-constexpr int kMaxAhead = 64;   // lookahead supported
+// history_len / lookahead up to these use per-thread local arrays; longer
+// windows use a per-thread slice of a global scratch buffer (same code).
+constexpr int kMaxHist = 64;
+constexpr int kMaxAhead = 64;
+
+// Per-window work arrays: h, y (H ints), raw (I), z and e (H + I), and the
+// least-squares design matrix A (5 (H - 3) rows-by-columns).
+struct Scratch {
+  int* h;
+  int* y;
+  double* raw;
+  double* z;
+  double* e;
+  double* A;
+};
+__host__ __device__ inline size_t scratch_doubles(int H, int I) {
+  return static_cast<size_t>(I) + 2 * static_cast<size_t>(H + I) + 5 * static_cast<size_t>(H) +
+         static_cast<size_t>(H);  // the last H doubles hold the 2H ints
+}
+__host__ __device__ inline Scratch scratch_at(double* base, int H, int I) {
+  Scratch sc;
+  sc.raw = base;
+  sc.z = sc.raw + I;
+  sc.e = sc.z + (H + I);
+  sc.A = sc.e + (H + I);
+  sc.h = reinterpret_cast<int*>(sc.A + 5 * static_cast<size_t>(H));
+  sc.y = sc.h + H;
+  return sc;
+}
 
 #define LP_HD __host__ __device__
 LP_HD __forceinline__ int iabs(int x) { return x < 0 ? -x : x; }
@@ -118,10 +145,9 @@ LP_HD bool least_squares(int m, const double* A, const double* b, double* x) {
 
 // arima_forecast (predictor.cpp:120-188): ARIMA(2,1,2) by two-stage least
 // squares on the differenced series; levels are damped cumulative sums.
-LP_HD bool arima(const int* h, int n, int ahead, double* out) {
+LP_HD bool arima(const int* h, int n, int ahead, double* out, double* z, double* e, double* A) {
   if (n < 5) return false;
   const int m = n - 1;
-  double z[kMaxHist + kMaxAhead], e[kMaxHist + kMaxAhead];
   bool any = false;
   for (int i = 1; i < n; ++i) {
     z[i - 1] = static_cast<double>(h[i] - h[i - 1]);
@@ -129,7 +155,6 @@ LP_HD bool arima(const int* h, int n, int ahead, double* out) {
   }
   if (!any) return false;
   const int rows = m - 2;  // t = 2 .. m-1
-  double A[kMaxHist * 5];
   for (int r = 0; r < rows; ++r) {
     const int t = r + 2;
     A[r * 3 + 0] = 1.0;
@@ -221,12 +246,12 @@ LP_HD void postprocess(const double* raw, int ahead, const lp_forecast_config& c
 
 // predict (predictor.cpp:239-274) for the history ending at counts[t].
 LP_HD void predict_one(const int32_t* counts, int t, const lp_forecast_config& cf, int method,
-                            const double* pw, int32_t* out) {
+                            const double* pw, int32_t* out, const Scratch& sc) {
   const int H = cf.history_len, I = cf.lookahead;
-  int h[kMaxHist];
+  int* h = sc.h;
   for (int i = 0; i < H; ++i) h[i] = counts[t - H + i];
   const int last = h[H - 1];
-  double raw[kMaxAhead];
+  double* raw = sc.raw;
   switch (method) {
     case LP_PREDICT_MOVING_AVG: {
       const int w = cf.moving_avg_window < H ? cf.moving_avg_window : H;
@@ -243,10 +268,10 @@ LP_HD void predict_one(const int32_t* counts, int t, const lp_forecast_config& c
       break;
     }
     case LP_PREDICT_ARIMA: {
-      int y[kMaxHist];
+      int* y = sc.y;
       for (int i = 0; i < H; ++i) y[i] = h[i];
       preprocess(y, H);
-      if (!arima(y, H, I, raw))
+      if (!arima(y, H, I, raw, sc.z, sc.e, sc.A))
         for (int k = 0; k < I; ++k) raw[k] = static_cast<double>(last);
       break;
     }
@@ -269,13 +294,20 @@ __device__ double l1_of(const int32_t* pred, const int32_t* actual, int len) {
 __global__ void predict_kernel(const int32_t* __restrict__ counts, int t_first, int n_windows,
                                lp_forecast_config cf, const int32_t* __restrict__ methods,
                                int n_methods, const double* __restrict__ pw, int32_t* __restrict__ preds,
-                               double* __restrict__ l1) {
+                               double* __restrict__ l1, double* __restrict__ gscratch) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_windows * n_methods) return;
   const int w = g / n_methods, mi = g % n_methods;
   const int t = t_first + w;
   int32_t* out = preds + static_cast<size_t>(g) * cf.lookahead;
-  predict_one(counts, t, cf, methods[mi], pw, out);
+  if (gscratch) {  // long windows: a slice of the global scratch buffer
+    const size_t per = scratch_doubles(cf.history_len, cf.lookahead);
+    predict_one(counts, t, cf, methods[mi], pw, out,
+                scratch_at(gscratch + static_cast<size_t>(g) * per, cf.history_len, cf.lookahead));
+  } else {
+    double local[kMaxAhead + 2 * (kMaxHist + kMaxAhead) + 5 * kMaxHist + kMaxHist];
+    predict_one(counts, t, cf, methods[mi], pw, out, scratch_at(local, cf.history_len, cf.lookahead));
+  }
   if (l1) l1[g] = l1_of(out, counts + t, cf.lookahead);
 }
 
@@ -301,8 +333,10 @@ lp_status run_windows(const int32_t* counts, int32_t len, int t_first, int n_win
     off += (b + 255) & ~size_t(255);
     return r;
   };
+  const bool big = cf.history_len > kMaxHist || cf.lookahead > kMaxAhead;
   const size_t o_c = take(4 * static_cast<size_t>(len)), o_m = take(4 * n_methods),
-               o_pw = take(8 * pw.size()), o_p = take(4 * nout * cf.lookahead), o_l = take(8 * nout);
+               o_pw = take(8 * pw.size()), o_p = take(4 * nout * cf.lookahead), o_l = take(8 * nout),
+               o_s = take(big ? 8 * nout * scratch_doubles(cf.history_len, cf.lookahead) : 0);
   unsigned char* d = nullptr;
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
@@ -319,7 +353,7 @@ lp_status run_windows(const int32_t* counts, int32_t len, int t_first, int n_win
   predict_kernel<<<blocks, threads, 0, st>>>(
       reinterpret_cast<int32_t*>(d + o_c), t_first, n_windows, cf, reinterpret_cast<int32_t*>(d + o_m),
       n_methods, reinterpret_cast<double*>(d + o_pw), reinterpret_cast<int32_t*>(d + o_p),
-      l1 ? reinterpret_cast<double*>(d + o_l) : nullptr);
+      l1 ? reinterpret_cast<double*>(d + o_l) : nullptr, big ? reinterpret_cast<double*>(d + o_s) : nullptr);
   cudaMemcpyAsync(preds, d + o_p, 4 * nout * cf.lookahead, cudaMemcpyDeviceToHost, st);
   if (l1) cudaMemcpyAsync(l1, d + o_l, 8 * nout, cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d, st);
@@ -332,8 +366,7 @@ lp_status run_windows(const int32_t* counts, int32_t len, int t_first, int n_win
 lp_status check_cfg(const lp_forecast_config* cf) {
   if (!cf) return pfail(LP_EINVAL, "predict: null config");
   if (cf->lookahead < 1) return pfail(LP_EINVAL, "predict: lookahead must be >= 1");
-  if (cf->history_len < 1 || cf->history_len > kMaxHist || cf->lookahead > kMaxAhead)
-    return pfail(LP_EUNSUPPORTED, "predict: history_len <= 64 and lookahead <= 64 are supported");
+  if (cf->history_len < 1) return pfail(LP_EINVAL, "predict: history_len must be >= 1");
   return LP_OK;
 }
 
@@ -343,7 +376,8 @@ lp_status check_cfg(const lp_forecast_config* cf) {
 void predict_host(const int32_t* counts, int t, const lp_forecast_config& cf, int method, int32_t* out) {
   std::vector<double> pw(cf.lookahead + 1);
   for (int e = 0; e <= cf.lookahead; ++e) pw[e] = std::pow(cf.steep_decay, e);
-  predict_one(counts, t, cf, method, pw.data(), out);
+  std::vector<double> sc(scratch_doubles(cf.history_len, cf.lookahead));
+  predict_one(counts, t, cf, method, pw.data(), out, scratch_at(sc.data(), cf.history_len, cf.lookahead));
 }
 }  // namespace lp
 

@@ -461,3 +461,22 @@ def test_infeasible_current_depth_keeps_later_levels():
         ref = plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns))
         assert got == ref, (cur, ns)
         p.close()
+
+
+@pytest.mark.parametrize("n,k", [(512, 300), (600, 300), (700, 420)])
+def test_k_above_255_matches_oracle(n, k):
+    """No k cap: more than 255 of n preempted with more than 255
+    pipelines per depth — the row kernel at n <= 512 (up to 10 bit planes),
+    the scenario-major kernel above (12-bit class counts)."""
+    w = resnet152_dp()  # P = 1 is feasible: depth 1 holds n pipelines
+    opt = PlannerOptions(mc_trials=3000)
+    p = planner(w, opt)
+    seed = O.planner_seed(0x5EED, n, k)
+    for c in [ParallelConfig(n, 1), ParallelConfig(n // 2, 2), ParallelConfig(n // 3, 3), ParallelConfig(n // 7, 7)]:
+        got, tot = p.survivor_counts(c, n, k)
+        want, wt = O.oracle_ensemble_counts(n, k, False, opt.mc_trials, seed, [c])
+        assert tot == wt and got.tolist() == want[0][: c.pipelines + 1].tolist(), c
+    ns = [n, n - k, n - k + 20]
+    plan = plan_rows(p.dp_optimize(ParallelConfig(n // 4, 4), ns))
+    assert plan == plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(ParallelConfig(n // 4, 4), ns))
+    p.close()

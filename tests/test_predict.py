@@ -77,3 +77,26 @@ def test_single_predict_and_errors():
         predict(trace[:5], cfg, "arima")  # history shorter than history_len
     with pytest.raises(ValueError):
         predict(trace[:30], cfg, "prophet")
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_long_windows_match_reference():
+    """No history / lookahead cap (both were capped at 64):
+    windows beyond the per-thread local arrays run from a global scratch
+    slice with the same code, bit-identical to the reference."""
+    import json
+    from pathlib import Path
+    trace = json.loads((Path(__file__).resolve().parents[1] / "tools" / "data" /
+                        "trace_gen_synthetic_128.json").read_text())["counts"][:900]
+    checked = 0
+    for H, I in [(100, 96), (240, 200), (64, 65), (65, 12)]:
+        cfg = ForecastConfig(history_len=H, lookahead=I, capacity=128)
+        preds, l1 = predict_windows(trace, cfg, METHODS)
+        assert len(preds) == len(trace) - H - I + 1
+        for w in range(0, len(preds), 37):
+            t = H + w
+            for m in range(len(METHODS)):
+                assert preds[w][m] == O.ref_predict(trace[t - H:t], cfg, m), (H, I, t, m)
+                checked += 1
+    assert checked > 200
