@@ -231,6 +231,7 @@ struct HistPlan {
   std::vector<WorkItem> work;
   std::vector<uint16_t> divtab;
   std::vector<uint32_t> dmask;  // bits kernel: per (range, pass, d) depth-divisor masks
+  size_t big_words = 0;         // n > kBigN: scratch words per thread of the big kernel
   std::vector<Group> groups;
   // Pipeline stages: pairs (and so entries, hist rows) are contiguous per
   // stage, in the order the DP first reads them.
@@ -507,6 +508,22 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     const uint64_t local = pd.t_hi - pd.t_lo;
     if (local == 0 || pd.n_entries == 0) continue;
     const int e_end = pd.entry_base + pd.n_entries;
+    if (pd.n > kBigN) {
+      // global-scratch kernel (lp_hist_big.cu): one range with every depth
+      int e_res = pd.entry_base, pmax = 1;
+      while (e_res < e_end && hp.entries[e_res].tmax >= 2) pmax = std::max(pmax, hp.entries[e_res++].P);
+      hp.big_words = std::max(hp.big_words, big_scratch_words(pd.n, pd.k, pmax));
+      hp.model_ops += local * 6ull * pd.k * (uint64_t)(e_res - pd.entry_base);
+      WorkItem w{};
+      w.pair = pi;
+      w.e_lo = pd.entry_base;
+      w.e_hi = e_end;
+      w.e_res_hi = e_res;
+      w.evt_lo = hp.entries[pd.entry_base].evt_off;
+      groups[{specs[pi].stage, 6, 0, kBigThreads, 0}].push_back(
+          {w, pd.t_lo, pd.t_hi, std::min<uint64_t>(per_block, 4096), 0, 0});
+      continue;
+    }
     if (!legacy && !rows_off && pd.k > kIncMaxK && pd.n <= 512 && (bits_off || pd.k > bits_max_k())) {
       // bit-sliced row kernel (lp_hist_rows.cu)
       const RowsShape& rs = rows_shape();
@@ -821,6 +838,9 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
 struct HistDev {
   const uint16_t* divtab;
   const uint32_t* dmask;
+  uint32_t* big_scratch;  // n > kBigN: per stage, grid x kBigThreads x big_words
+  size_t big_words;
+  int big_grid;
   const PairDesc* pairs;
   const EntryDesc* entries;
   const DrawConst* draws;
@@ -841,7 +861,11 @@ cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int*
   if (e != cudaSuccess) return e;
   for (const Group& g : hp.groups) {
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 5)
+    if (g.kind == 6)
+      e = launch_hist_big(g.count, d.big_grid, st, w, d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0,
+                          d.big_scratch + (size_t)g.stage * d.big_grid * kBigThreads * d.big_words,
+                          d.big_words);
+    else if (g.kind == 5)
       e = launch_hist_bits(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
@@ -875,7 +899,11 @@ cudaError_t run_hist_stage(const HistPlan& hp, const HistDev& d, cudaStream_t st
   for (const Group& g : hp.groups) {
     if (g.stage != stage) continue;
     const WorkItem* w = d.work + g.first;
-    if (g.kind == 5)
+    if (g.kind == 6)
+      e = launch_hist_big(g.count, d.big_grid, st, w, d.pairs, d.entries, d.draws, d.binom, d.evt, d.h0,
+                          d.big_scratch + (size_t)g.stage * d.big_grid * kBigThreads * d.big_words,
+                          d.big_words);
+    else if (g.kind == 5)
       e = launch_hist_bits(g.kmax, g.smem_evt, g.count, g.threads, g.smem, st, w,
                            d.pairs, d.entries, d.draws, d.binom, d.dmask, d.evt, d.h0);
     else if (g.kind == 4)
@@ -1002,6 +1030,7 @@ struct lp_handle {
   int dp_staged_nprob = -1;  // >= 0: this re-plan's persistent DP runs staged
   int dp_staged_kb = 100;    // shared-memory budget of the staged DP (LIVEPUT_DP_STAGED_KB)
   DevBuf tables, work;
+  DevBuf big_scratch;  // lp_hist_big.cu scratch (n > kBigN only)
   PinBuf pin_up, pin_down;
   size_t up_bytes = 0;
   lp_stats stats{};
@@ -1065,6 +1094,18 @@ T* dptr(DevBuf& b, size_t off) {
 }
 
 // Builds and uploads a hist plan into (tables, work); returns device ptrs.
+// Scratch of the big-n kernel: one slice per (stage, thread of its grid).
+lp_status bind_big_scratch(lp_handle* h, const HistPlan& hp, HistDev& d) {
+  d.big_words = hp.big_words;
+  d.big_grid = std::max(1, h->num_sms);
+  d.big_scratch = nullptr;
+  if (hp.big_words == 0) return LP_OK;
+  const size_t bytes = 4 * hp.big_words * (size_t)d.big_grid * kBigThreads * std::max<size_t>(hp.stages.size(), 1);
+  LP_CUDA(h, h->big_scratch.ensure(bytes));
+  d.big_scratch = static_cast<uint32_t*>(h->big_scratch.p);
+  return LP_OK;
+}
+
 lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& work, HistDev& d,
                       Packer& pk, std::vector<size_t>& extra_offs) {
   (void)extra_offs;
@@ -1086,6 +1127,10 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
   d.work = dptr<WorkItem>(tables, ow);
   d.divtab = dptr<uint16_t>(tables, odt);
   d.dmask = dptr<uint32_t>(tables, odm);
+  {
+    lp_status bs = bind_big_scratch(h, hp, d);
+    if (bs != LP_OK) return bs;
+  }
   d.evt = dptr<uint32_t>(work, 0);
   d.h0 = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)));
   d.hist = dptr<uint32_t>(work, a16(4 * std::max<int64_t>(hp.evt_len, 1)) +
@@ -1240,7 +1285,7 @@ const char* lp_last_error(const lp_handle* h) { return h ? h->err.c_str() : g_gl
 int32_t lp_max_instances(void) { return kMaxN; }
 
 const char* lp_build_info(void) {
-  return "liveput sm_100a (tcgen05-free integer/FP64 path); kMaxN=2048; variants R(k<=16) C(k<=255)";
+  return "liveput sm_100a (tcgen05-free integer/FP64 path); kMaxN=16384 (global-scratch kernel past 2048); any k";
 }
 
 lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_options* options,
@@ -1834,6 +1879,10 @@ lp_status exec_hist(lp_handle* h) {
   d.work = dptr<WorkItem>(h->tables, h->off_work);
   d.divtab = dptr<uint16_t>(h->tables, h->off_divtab);
   d.dmask = dptr<uint32_t>(h->tables, h->off_dmask);
+  {
+    lp_status bs = bind_big_scratch(h, h->hp, d);
+    if (bs != LP_OK) return bs;
+  }
   d.evt = dptr<uint32_t>(h->work, h->w_evt);
   d.h0 = dptr<uint32_t>(h->work, h->w_h0);
   d.hist = dptr<uint32_t>(h->work, h->w_hist);

@@ -27,6 +27,13 @@ cudaError_t launch_hist_inc(int kmax, bool smem_evt, int blocks, int threads, si
                             cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
                             const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,
                             const uint16_t* divtab, uint32_t* evt, uint32_t* h0);
+// n > kBigN: every per-thread array in a global scratch slice (lp_hist_big.cu)
+constexpr int kBigN = 2048;
+constexpr int kBigThreads = 64;
+size_t big_scratch_words(int n, int k, int pmax);
+cudaError_t launch_hist_big(int n_items, int grid, cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
+                            const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
+                            uint32_t* h0, uint32_t* scratch, size_t per_thread);
 cudaError_t launch_hist_bits(int kmax, bool smem_evt, int blocks, int threads, size_t smem,
                              cudaStream_t st, const WorkItem* w, const PairDesc* pairs,
                              const EntryDesc* ents, const DrawConst* dr, const uint64_t* binom,

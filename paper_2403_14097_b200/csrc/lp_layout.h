@@ -18,7 +18,7 @@
 
 namespace lp {
 
-constexpr int kMaxN = 2048;     // instances per availability count (u16 slot ids)
+constexpr int kMaxN = 16384;    // instances per availability count (u16 slot ids; > 2048: lp_hist_big.cu)
 constexpr int kMaxKReg = 16;    // register-resident scenarios (variant R)
 constexpr int kMaxK = 255;      // u8 class counters (variant C)
 constexpr int kComb = 4;        // scenario-major kernel: Dmax <= kComb uses the bitmap comb

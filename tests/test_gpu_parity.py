@@ -294,7 +294,7 @@ def test_errors():
     with pytest.raises(ValueError):
         p.sequence_value(None, [None], [8, 8, 8])
     with pytest.raises(LiveputError):
-        p.dp_optimize(None, [4096, 4000])
+        p.dp_optimize(None, [20000, 19990])  # n beyond kMaxN = 16384: LP_EUNSUPPORTED
     p.close()
     p = planner(lm_1p5b(), PlannerOptions(mc_trials=0))
     with pytest.raises(ValueError):
@@ -480,3 +480,28 @@ def test_k_above_255_matches_oracle(n, k):
     plan = plan_rows(p.dp_optimize(ParallelConfig(n // 4, 4), ns))
     assert plan == plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(ParallelConfig(n // 4, 4), ns))
     p.close()
+
+
+@pytest.mark.parametrize("n,k", [(3000, 5), (3000, 60), (4096, 1500), (16384, 24)])
+def test_beyond_2048_instances_vs_oracle(n, k):
+    """n up to 16384 (n > 2048 was refused): the global-scratch
+    kernel (lp_hist_big.cu) against the cache-free oracle, and a one-interval
+    re-plan at n = 3000."""
+    w = resnet152_dp()
+    trials = 600
+    p = planner(w, PlannerOptions(mc_trials=trials, exact_cap=0))
+    sel = [ParallelConfig(n, 1), ParallelConfig(n // 2, 2), ParallelConfig(n // 13, 13), ParallelConfig(7, n // 7),
+           ParallelConfig(1, n)]
+    ref, tot = O.oracle_ensemble_counts(n, k, False, trials, O.planner_seed(0x5EED, n, k), sel)
+    for ci, c in enumerate(sel):
+        got, gt = p.survivor_counts(c, n, k)
+        assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, c)
+    p.close()
+    if n == 3000:
+        opt = PlannerOptions(mc_trials=300)
+        ns = [n, n - k]
+        cur = ParallelConfig(n // 10, 10)
+        want = plan_rows(O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns))
+        q = planner(w, opt)
+        assert plan_rows(q.dp_optimize(cur, ns)) == want
+        q.close()
