@@ -396,6 +396,18 @@ static int ensemble_range(int n, int k, int exact, int trials, uint64_t seed, co
 }
 
 /* ---- Planner ------------------------------------------------------------ */
+/* Optional memo of full-level ensembles (or_planner_set_cache): the
+ * reference's hist_cache_ (optimizer.hpp:88) for long replays.  Keyed by
+ * (n_now, k); holds the counts of every config of n_now (enumerate_configs
+ * order), so a re-plan's levels j >= 1 — whose prev nodes are exactly those
+ * configs — reuse them.  Values are identical with the memo on or off. */
+typedef struct {
+  int n, k, nc, stride;
+  int* cfg; /* nc (D, P) pairs */
+  uint64_t* counts;
+  uint64_t total;
+} or_memo;
+
 struct or_planner {
   lp_profile w;
   int32_t* depths;
@@ -403,6 +415,9 @@ struct or_planner {
   lp_costs c;
   lp_options o;
   int threads;
+  int cache_on;
+  or_memo* memo;
+  int n_memo, cap_memo;
 };
 
 or_planner* or_planner_new(const lp_profile* w, const lp_costs* c, const lp_options* o,
@@ -423,8 +438,15 @@ or_planner* or_planner_new(const lp_profile* w, const lp_costs* c, const lp_opti
   return pl;
 }
 
+void or_planner_set_cache(or_planner* pl, int on) { pl->cache_on = on; }
+
 void or_planner_free(or_planner* pl) {
   if (!pl) return;
+  for (int i = 0; i < pl->n_memo; ++i) {
+    free(pl->memo[i].cfg);
+    free(pl->memo[i].counts);
+  }
+  free(pl->memo);
   free(pl->depths);
   free(pl->rates);
   free(pl);
@@ -520,6 +542,52 @@ int or_liveput(or_planner* pl, int d, int p, int n_now, int n_minus, double* out
   return 0;
 }
 
+/* Counts of the configs pc[0..nc) at (n_now, k) from the memo of the full
+ * config list of n_now (computed on first use); 0 on success, -1 when some
+ * config is not a config of n_now (e.g. an infeasible `current`). */
+static int memo_counts(or_planner* pl, const int* pc, int nc, int n_now, int k, uint64_t* counts,
+                       int stride, uint64_t* total) {
+  or_memo* m = NULL;
+  for (int i = 0; i < pl->n_memo; ++i)
+    if (pl->memo[i].n == n_now && pl->memo[i].k == k) m = &pl->memo[i];
+  if (!m) {
+    const int cnt = or_enumerate_configs(&pl->w, n_now, NULL, 0);
+    if (cnt <= 0) return -1;
+    if (pl->n_memo == pl->cap_memo) {
+      pl->cap_memo = pl->cap_memo ? 2 * pl->cap_memo : 16;
+      pl->memo = (or_memo*)realloc(pl->memo, sizeof(or_memo) * pl->cap_memo);
+    }
+    m = &pl->memo[pl->n_memo];
+    m->n = n_now;
+    m->k = k;
+    m->nc = cnt;
+    m->cfg = (int*)malloc(sizeof(int) * 2 * cnt);
+    or_enumerate_configs(&pl->w, n_now, m->cfg, cnt);
+    int md = 0;
+    for (int i = 0; i < cnt; ++i) md = m->cfg[2 * i] > md ? m->cfg[2 * i] : md;
+    m->stride = md + 1;
+    m->counts = (uint64_t*)calloc((size_t)cnt * m->stride, sizeof(uint64_t));
+    if (planner_counts(pl, m->cfg, cnt, n_now, k, m->counts, m->stride, &m->total) != 0) {
+      free(m->cfg);
+      free(m->counts);
+      return -1;
+    }
+    ++pl->n_memo;
+  }
+  for (int c = 0; c < nc; ++c) {
+    int row = -1;
+    for (int i = 0; i < m->nc; ++i)
+      if (m->cfg[2 * i] == pc[2 * c] && m->cfg[2 * i + 1] == pc[2 * c + 1]) {
+        row = i;
+        break;
+      }
+    if (row < 0) return -1;
+    for (int d = 0; d < stride; ++d) counts[(size_t)c * stride + d] = d <= pc[2 * c] ? m->counts[(size_t)row * m->stride + d] : 0;
+  }
+  *total = m->total;
+  return 0;
+}
+
 typedef struct {
   int d, p;
   double value, mig;
@@ -564,7 +632,9 @@ int or_dp_optimize(or_planner* pl, int cd, int cp, const int* n_seq, int len, in
     const int stride = maxd + 1;
     uint64_t* counts = (uint64_t*)calloc((size_t)(nc > 0 ? nc : 1) * stride, sizeof(uint64_t));
     uint64_t total = 0;
-    if (nc > 0 && planner_counts(pl, pc, nc, n_now, k, counts, stride, &total) != 0) {
+    if (nc > 0 && pl->cache_on && memo_counts(pl, pc, nc, n_now, k, counts, stride, &total) == 0) {
+      /* served from the memo */
+    } else if (nc > 0 && planner_counts(pl, pc, nc, n_now, k, counts, stride, &total) != 0) {
       free(pc);
       free(map);
       free(counts);

@@ -71,6 +71,9 @@ typedef struct or_planner or_planner;
 or_planner* or_planner_new(const lp_profile* w, const lp_costs* c, const lp_options* o,
                            int threads);
 void or_planner_free(or_planner* pl);
+/* opt-in memo of full-level ensembles per (n_now, k) for long replays (the
+ * reference's hist_cache_); results are identical with it on or off */
+void or_planner_set_cache(or_planner* pl, int on);
 const char* or_last_error(void);
 int or_survivor_counts(or_planner* pl, int d, int p, int n_now, int n_minus, uint64_t* counts,
                        uint64_t* total);

@@ -66,6 +66,7 @@ def oracle_lib():
                                                    C.c_longlong, C.c_longlong]),
             "or_planner_new": (C.c_void_p, [prof, costs, opts, C.c_int]),
             "or_planner_free": (None, [C.c_void_p]),
+            "or_planner_set_cache": (None, [C.c_void_p, C.c_int]),
             "or_last_error": (C.c_char_p, []),
             "or_survivor_counts": (C.c_int, [C.c_void_p] + [C.c_int] * 4 + [_P(C.c_uint64), _P(C.c_uint64)]),
             "or_phi": (C.c_int, [C.c_void_p] + [C.c_int] * 6 + [_P(C.c_double)]),
@@ -205,11 +206,13 @@ class RefPlanner(_PlannerBase):
 class OraclePlanner(_PlannerBase):
     """The C restatement (cache-free) — used where the reference is absent or aliases."""
 
-    def __init__(self, w, costs=None, opt=None, threads: int = 0):
+    def __init__(self, w, costs=None, opt=None, threads: int = 0, cache: bool = False):
         super().__init__(w, costs or CostTable(), opt or PlannerOptions())
         self.L = oracle_lib()
         threads = threads or min(8, os.cpu_count() or 1)
         self.h = self.L.or_planner_new(C.byref(self._p), C.byref(self._c), C.byref(self._o), threads)
+        if cache:  # memo of full-level ensembles for long replays (identical results)
+            self.L.or_planner_set_cache(self.h, 1)
 
     def __del__(self):
         if getattr(self, "h", None):
