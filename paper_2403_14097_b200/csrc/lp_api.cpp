@@ -1028,6 +1028,7 @@ struct lp_handle {
   bool dp_launches = false;  // LIVEPUT_DP=launches: one kernel per level (A/B)
   bool dp_staged = true;     // LIVEPUT_DP_STAGED=0: never stage the DP in shared memory (A/B)
   int dp_staged_nprob = -1;  // >= 0: this re-plan's persistent DP runs staged
+  bool dp_cluster = false;   // ... as the 8-CTA cluster kernel (small re-plans)
   int dp_staged_kb = 100;    // shared-memory budget of the staged DP (LIVEPUT_DP_STAGED_KB)
   DevBuf tables, work;
   DevBuf big_scratch;  // lp_hist_big.cu scratch (n > kBigN only)
@@ -1841,6 +1842,7 @@ lp_status prepare_dp(lp_handle* h) {
   // shared-memory staged persistent DP (lp_dp.cu) when the whole DP input
   // fits in a block's shared memory next to 3 more blocks per SM
   h->dp_staged_nprob = -1;
+  h->dp_cluster = false;
   if (h->dp_staged && H <= 64) {
     long long nprob = 0;
     for (int j = 0; j < H; ++j) {
@@ -1850,6 +1852,16 @@ lp_status prepare_dp(lp_handle* h) {
     const int n_nodes = h->levels[H - 1].next_base + h->levels[H - 1].next_count;
     if (nprob < (1 << 20) && dp_staged_smem(n_nodes, H, (int)nprob) <= (size_t)h->dp_staged_kb * 1024)
       h->dp_staged_nprob = (int)nprob;
+    // the cluster DP (one 8-CTA cluster, DSMEM level values) for the smallest
+    // re-plans; LIVEPUT_DP_CLUSTER=0 disables, LIVEPUT_DP_CLUSTER_MAXNEXT caps
+    static const int cluster_max_next = [] {
+      const char* e = getenv("LIVEPUT_DP_CLUSTER");
+      if (e && e[0] == '0') return 0;
+      const char* m = getenv("LIVEPUT_DP_CLUSTER_MAXNEXT");
+      return m ? atoi(m) : 128;
+    }();
+    h->dp_cluster = h->dp_staged_nprob >= 0 && h->max_next <= cluster_max_next &&
+                    dp_cluster_smem(n_nodes, H, (int)nprob) <= 200 * 1024;
   }
   size_t bytes = 0;
   lp_status us = upload_image(h,
@@ -1987,8 +1999,11 @@ lp_status exec_dp(lp_handle* h) {
       a.trace = static_cast<uint64_t*>(h->dp_trace.p);
     }
     const LevelDesc& last = h->levels[h->horizon - 1];
-    LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S,
-                                    last.next_base + last.next_count, h->dp_staged_nprob));
+    if (h->dp_cluster)
+      LP_CUDA(h, launch_dp_cluster(st, a, h->S, last.next_base + last.next_count, h->dp_staged_nprob));
+    else
+      LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S,
+                                      last.next_base + last.next_count, h->dp_staged_nprob));
     ++launches;
   } else {
     LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0

@@ -15,6 +15,7 @@
 // (value desc, mig asc, first index) argmax is a warp-shuffle + cross-warp
 // reduction.  The winning value, migration total, back-pointer and step terms
 // of every node stay in HBM for the traceback.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -911,6 +912,234 @@ cudaError_t launch_dp_persistent(int device, int num_sms, int max_next, cudaStre
   StagedLayout gg = G;
   void* params[] = {&aa, &ss, &gg};
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(256), params, smem, st);
+}
+
+
+// ---------------------------------------------------------------------------
+// Cluster DP for small re-plans (round 2).  One thread-block cluster of
+// kClusterCtas CTAs runs normalisation, every level, the final pick and the
+// traceback.  Levels are separated by barrier.cluster (release/acquire at
+// cluster scope) instead of a grid barrier through global atomics, and the
+// level values travel through distributed shared memory: the warp that
+// decides node c' stores (F, M) of c' into every CTA's table, so the next
+// level reads them from its own shared memory.  One warp per next node: its
+// lanes stride over the prev nodes and reduce the take-order key with
+// shuffles, with no block barrier inside a level.  Every CTA stages the node
+// list, the per-node cost terms and every prev probability row up front, so
+// a level touches no global memory except the back-pointer writes.
+namespace cg = cooperative_groups;
+
+struct ClusterLayout {
+  int n_nodes, horizon, n_prob;
+  __host__ __device__ size_t cfg_off() const { return 0; }
+  __host__ __device__ size_t lv_off() const { return (size_t)n_nodes * sizeof(NodeCfg); }
+  __host__ __device__ size_t nc_off() const {
+    return (lv_off() + (size_t)horizon * sizeof(LevelDesc) + 15) & ~static_cast<size_t>(15);
+  }
+  __host__ __device__ size_t vm_off() const { return nc_off() + (size_t)n_nodes * sizeof(NodeCost); }
+  __host__ __device__ size_t base_off() const { return vm_off() + (size_t)n_nodes * sizeof(double2); }
+  __host__ __device__ size_t prob_off() const {
+    return (base_off() + (size_t)(horizon + 1) * sizeof(int) + 15) & ~static_cast<size_t>(15);
+  }
+  __host__ __device__ size_t bytes() const { return prob_off() + (size_t)n_prob * sizeof(double); }
+};
+
+constexpr int kClusterCtas = 8;
+constexpr int kClusterThreads = 256;
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, 1)
+    dp_cluster_kernel(DpArgs a, DpScalars S, ClusterLayout G) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  __shared__ int s_idx[kClusterThreads];
+  __shared__ int s_path[kMaxHorizon + 1];
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  NodeCfg* s_cfg = reinterpret_cast<NodeCfg*>(sm_raw + G.cfg_off());
+  LevelDesc* s_lv = reinterpret_cast<LevelDesc*>(sm_raw + G.lv_off());
+  NodeCost* s_nc = reinterpret_cast<NodeCost*>(sm_raw + G.nc_off());
+  double2* s_vm = reinterpret_cast<double2*>(sm_raw + G.vm_off());
+  int* s_base = reinterpret_cast<int*>(sm_raw + G.base_off());
+  double* s_prob = reinterpret_cast<double*>(sm_raw + G.prob_off());
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = kClusterThreads / 32;
+
+  // tables: node list, level descriptors, every next-role node's cost terms
+  // (level 0's `current` is never a next node, and its depth may have no
+  // throughput or cost row)
+  const int first_next = a.levels[0].next_base;
+  for (int i = threadIdx.x; i < G.n_nodes; i += blockDim.x) {
+    const NodeCfg nx = a.cfg[i];
+    s_cfg[i] = nx;
+    NodeCost nc{0.0, 0.0, 0.0, 0.0};
+    if (nx.d > 0 && i >= first_next) {
+      const double4 pc = a.pcost[nx.p];
+      nc.thr = a.thr_tab[a.thr_row[nx.p] + nx.d];
+      nc.pipe = pc.x;
+      nc.unit = pc.y;
+      nc.resume = pc.z;
+    }
+    s_nc[i] = nc;
+  }
+  for (int j = threadIdx.x; j < G.horizon; j += blockDim.x) s_lv[j] = a.levels[j];
+  if (threadIdx.x == 0) s_vm[0] = make_double2(0.0, 0.0);  // level 0: value 0, migration 0
+  // phase 0: probabilities of the fresh entries, split over the cluster
+  for (int e = rank; e < a.n_entries; e += kClusterCtas) {
+    const EntryDesc en = a.entries[e];
+    const PairDesc pd = a.pairs[en.pair];
+    const int len = hist_row(en.Dmax + 1, pd.k);
+    const double total = static_cast<double>(pd.count);
+    double* out = a.store + a.store_off[e];
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint32_t c = a.hist[en.hist_off + i];
+      out[i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
+    }
+  }
+  __threadfence();
+  cluster.sync();  // the store is complete (every CTA's normalisation)
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int j = 0; j < G.horizon; ++j) {
+      s_base[j] = b;
+      const LevelDesc& L = s_lv[j];
+      if (L.has_hist) b += L.prev_count * (min(L.k, L.n_now) + 1);
+    }
+    s_base[G.horizon] = b;
+  }
+  __syncthreads();
+  {  // every prev row the DP reads (L2 reads: written by peer CTAs)
+    const int n_prev = s_lv[G.horizon - 1].next_base;
+    for (int gi = threadIdx.x; gi < n_prev; gi += blockDim.x) {
+      int j = 0;
+      while (j + 1 < G.horizon && s_lv[j + 1].prev_base <= gi) ++j;
+      const LevelDesc& L = s_lv[j];
+      const NodeCfg pv = s_cfg[gi];
+      if (!L.has_hist || pv.d <= 0 || pv.hist_off < 0) continue;
+      const int stride = min(L.k, L.n_now) + 1, len = min(L.k, pv.d) + 1;
+      const double* src = a.store + pv.hist_off;
+      double* dst = s_prob + s_base[j] + (gi - L.prev_base) * stride;
+      for (int d = 0; d < len; ++d) dst[d] = __ldcg(src + d);
+    }
+  }
+  __syncthreads();
+
+  // levels: one warp per next node
+  for (int j = 0; j < G.horizon; ++j) {
+    const LevelDesc L = s_lv[j];
+    const int stride = min(L.k, L.n_now) + 1;
+    for (int nb = rank * nwarps + warp; nb < L.next_count; nb += kClusterCtas * nwarps) {
+      const int ni = L.next_base + nb;
+      const NodeCfg nx = s_cfg[ni];
+      const NodeCost nc = s_nc[ni];
+      const PhiConst K = phi_const(L, S, nc);
+      Cand best{0.0, 0.0, 0.0, 0.0, -1};
+      for (int pi = lane; pi < L.prev_count; pi += 32) {
+        const int gi = L.prev_base + pi;
+        const NodeCfg pv = s_cfg[gi];
+        const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{s_prob + s_base[j] + pi * stride}, a.thr_tab,
+                                  a.thr_row, K);
+        const double2 vm = s_vm[gi];
+        const double v = __dadd_rn(vm.x, ph.committed);
+        const double mg = __dadd_rn(vm.y, ph.mig);
+        if (best.idx < 0 || v > best.value ||
+            (v == best.value && (mg < best.mig || (mg == best.mig && pi < best.idx)))) {
+          best.value = v;
+          best.mig = mg;
+          best.stc = ph.committed;
+          best.stm = ph.mig;
+          best.idx = pi;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const Cand o = shfl_cand(best, lane ^ off);
+        if (cand_better(o, best)) best = o;
+      }
+      // every lane holds the winner: lanes 0..kClusterCtas-1 store (F, M)
+      // into their CTA's table; lane 0 also writes the traceback terms
+      if (lane < kClusterCtas) {
+        double2* dst = cluster.map_shared_rank(s_vm, lane);
+        dst[ni] = make_double2(best.value, best.mig);
+      }
+      if (lane == 0) {
+        __stcg(a.val + ni, best.value);
+        __stcg(a.mig + ni, best.mig);
+        __stcg(a.parent + ni, best.idx);
+        __stcg(a.stc + ni, best.stc);
+        __stcg(a.stm + ni, best.stm);
+      }
+    }
+    __threadfence();
+    cluster.sync();
+  }
+
+  // final pick (rank = (value, -mig, D, -P), suspended as (-1, 0), first
+  // index wins) and traceback, by CTA 0
+  if (rank != 0) return;
+  const LevelDesc last = s_lv[G.horizon - 1];
+  const int base = last.next_base, cnt = last.next_count;
+  auto gt = [&](int x, int y) -> bool {  // rank(x) > rank(y)
+    if (y < 0) return x >= 0;
+    if (x < 0) return false;
+    const double va = s_vm[base + x].x, vb = s_vm[base + y].x;
+    if (vb < va) return true;
+    if (va < vb) return false;
+    const double ma = -s_vm[base + x].y, mb = -s_vm[base + y].y;
+    if (mb < ma) return true;
+    if (ma < mb) return false;
+    const NodeCfg ca = s_cfg[base + x], cb = s_cfg[base + y];
+    const int da = ca.d > 0 ? ca.d : -1, db = cb.d > 0 ? cb.d : -1;
+    if (db < da) return true;
+    if (da < db) return false;
+    const int pa = ca.d > 0 ? -ca.p : 0, pb = cb.d > 0 ? -cb.p : 0;
+    return pb < pa;
+  };
+  int mine = -1;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    if (gt(i, mine)) mine = i;  // ascending i: strict > keeps the first
+  s_idx[threadIdx.x] = mine;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      const int x = s_idx[threadIdx.x], y = s_idx[threadIdx.x + st];
+      if (gt(y, x) || (y >= 0 && x >= 0 && !gt(x, y) && y < x)) s_idx[threadIdx.x] = y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int idx = s_idx[0];
+    if (a.final_value) *a.final_value = s_vm[base + idx].x;
+    for (int jj = G.horizon; jj >= 1; --jj) {
+      const int gi = s_lv[jj - 1].next_base + idx;
+      s_path[jj] = gi;
+      idx = __ldcg(a.parent + gi);
+    }
+  }
+  __syncthreads();
+  for (int jj = 1 + threadIdx.x; jj <= G.horizon; jj += blockDim.x) {
+    const int gi = s_path[jj];
+    const NodeCfg c = s_cfg[gi];
+    lp_plan_step st;
+    st.interval_index = jj;
+    st.config.pipelines = c.d > 0 ? c.d : 0;
+    st.config.stages = c.d > 0 ? c.p : 0;
+    st.expected_committed = __ldcg(a.stc + gi);
+    st.expected_mig_cost_s = __ldcg(a.stm + gi);
+    a.plan[jj - 1] = st;
+  }
+}
+
+size_t dp_cluster_smem(int n_nodes, int horizon, int n_prob) {
+  return ClusterLayout{n_nodes, horizon, n_prob}.bytes();
+}
+
+cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob) {
+  if (a.horizon > kMaxHorizon) return cudaErrorInvalidValue;
+  const ClusterLayout G{n_nodes, a.horizon, n_prob};
+  const size_t smem = G.bytes();
+  cudaError_t e = smem_optin(reinterpret_cast<const void*>(dp_cluster_kernel), smem);
+  if (e != cudaSuccess) return e;
+  dp_cluster_kernel<<<kClusterCtas, kClusterThreads, smem, st>>>(a, S, G);
+  return cudaGetLastError();
 }
 
 }  // namespace lp
