@@ -12,8 +12,8 @@ reference-vs-restatement legs of make_plans_1e6.py.
   config3i  GPT-3 6.7B, N=128, the 1440-interval trace, the same Ideal(12) loop
   config3p  the same trace with Proactive(12, arima): n_seq = [n] + predict() of the
             history left-padded to 12 (the reference's predictor via oracle/_ref)
-  sweep     config 5: N in {16..256} x I in {4..32} (tools/sweep.py availability), and
-            N = 512 for I <= 8; full plans
+  sweep     config 5: N in {16..512} x I in {4..32} (tools/sweep.py availability);
+            full plans (points already in the file are kept)
 
 Each re-plan stores (current, n_seq, first step); sweep points store the whole plan.
 Run in the dev container (the Proactive forecasts need oracle/_ref):
@@ -91,13 +91,14 @@ def config3(proactive):
             "trace": "tools/data/trace_gen_synthetic_128.json", "replans": seq}
 
 
-def sweep():
+def sweep(done=()):
     import sweep as SW
     w = lm_1p5b()
-    pts = []
+    pts = list(done)
+    have = {(p["n"], p["I"]) for p in pts}
     for n in SW.NS:
         for I in SW.IS:
-            if n == 512 and I > 8:
+            if (n, I) in have:
                 continue
             ns = SW.availability(n, I)
             cur = O.oracle_reactive(w, ns[0])
@@ -106,6 +107,9 @@ def sweep():
                                    cache=True).dp_optimize(cur, ns)
             pts.append({"n": n, "I": I, "current": enc_cfg(cur), "n_seq": ns, "plan": [enc_step(s) for s in plan]})
             print(f"sweep N={n} I={I}: {time.perf_counter() - t:.1f} s", flush=True)
+            OUT.write_text(json.dumps({**json.loads(OUT.read_text()),
+                                       "sweep": {"profile": "lm_1p5b", "trials": TRIALS, "points": pts}},
+                                      separators=(",", ":")))
     return {"profile": "lm_1p5b", "trials": TRIALS, "points": pts}
 
 
@@ -116,7 +120,7 @@ def main():
     only = set(x for x in a.only.split(",") if x)
     data = json.loads(OUT.read_text()) if OUT.exists() else {}
     jobs = {"config2": config2, "config3i": lambda: config3(False), "config3p": lambda: config3(True),
-            "sweep": sweep}
+            "sweep": lambda: sweep(data.get("sweep", {}).get("points", []))}
     for k, fn in jobs.items():
         if only and k not in only:
             continue
