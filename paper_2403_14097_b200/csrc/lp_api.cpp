@@ -1861,7 +1861,8 @@ lp_status prepare_dp(lp_handle* h) {
       return m ? atoi(m) : 128;
     }();
     h->dp_cluster = h->dp_staged_nprob >= 0 && h->max_next <= cluster_max_next &&
-                    dp_cluster_smem(n_nodes, H, (int)nprob) <= 200 * 1024;
+                    dp_cluster_smem(n_nodes, H, (int)nprob, (int)h->pcost.size(), (int)h->thr.row.size(),
+                                    (int)h->thr.vals.size()) <= 200 * 1024;
   }
   size_t bytes = 0;
   lp_status us = upload_image(h,
@@ -2000,7 +2001,8 @@ lp_status exec_dp(lp_handle* h) {
     }
     const LevelDesc& last = h->levels[h->horizon - 1];
     if (h->dp_cluster)
-      LP_CUDA(h, launch_dp_cluster(st, a, h->S, last.next_base + last.next_count, h->dp_staged_nprob));
+      LP_CUDA(h, launch_dp_cluster(st, a, h->S, last.next_base + last.next_count, h->dp_staged_nprob,
+                                   (int)h->pcost.size(), (int)h->thr.row.size(), (int)h->thr.vals.size()));
     else
       LP_CUDA(h, launch_dp_persistent(h->device, h->num_sms, h->max_next, st, a, h->S,
                                       last.next_base + last.next_count, h->dp_staged_nprob));
@@ -2107,6 +2109,10 @@ lp_status lp_fetch(lp_handle* h, lp_plan_step* out, lp_liveput_row* live, int32_
     cudaMemcpy(tr.data(), h->dp_trace.p, tr.size() * 8, cudaMemcpyDeviceToHost);
     int used = 0;
     while ((size_t)used < nb && tr[(size_t)used * per] != 0) ++used;
+    if (used > 0 && tr[1] && tr[0])
+      fprintf(stderr, "[dp] block 0: start -> first level %.2f us, kernel span %.2f us\n",
+              (double)(tr[1] - tr[0]) * 1e-3,
+              (double)(tr[3 + 2 * (std::min(h->horizon, kTraceLevels) - 1)] - tr[0]) * 1e-3);
     for (int j = 1; j < std::min(h->horizon, kTraceLevels); ++j) {
       uint64_t smin = UINT64_MAX, emax = 0;
       std::vector<double> comp;

@@ -931,6 +931,7 @@ namespace cg = cooperative_groups;
 
 struct ClusterLayout {
   int n_nodes, horizon, n_prob;
+  int n_pcost, n_throw, n_thr;  // per-depth cost terms, throughput rows and values
   __host__ __device__ size_t cfg_off() const { return 0; }
   __host__ __device__ size_t lv_off() const { return (size_t)n_nodes * sizeof(NodeCfg); }
   __host__ __device__ size_t nc_off() const {
@@ -941,7 +942,12 @@ struct ClusterLayout {
   __host__ __device__ size_t prob_off() const {
     return (base_off() + (size_t)(horizon + 1) * sizeof(int) + 15) & ~static_cast<size_t>(15);
   }
-  __host__ __device__ size_t bytes() const { return prob_off() + (size_t)n_prob * sizeof(double); }
+  __host__ __device__ size_t pc_off() const {
+    return (prob_off() + (size_t)n_prob * sizeof(double) + 15) & ~static_cast<size_t>(15);
+  }
+  __host__ __device__ size_t tt_off() const { return pc_off() + (size_t)n_pcost * sizeof(double4); }
+  __host__ __device__ size_t tr_off() const { return tt_off() + (size_t)n_thr * sizeof(double); }
+  __host__ __device__ size_t bytes() const { return tr_off() + (size_t)n_throw * sizeof(int); }
 };
 
 constexpr int kClusterCtas = 8;
@@ -962,25 +968,41 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
   double* s_prob = reinterpret_cast<double*>(sm_raw + G.prob_off());
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = kClusterThreads / 32;
+  auto stamp = [&](int slot) {  // LIVEPUT_DP_TRACE: per-CTA globaltimer stamps
+    if (a.trace && threadIdx.x == 0 && slot < 2 * kTraceLevels + 2) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      a.trace[(size_t)rank * (2 * kTraceLevels + 2) + slot] = t;
+    }
+  };
+  stamp(0);
 
-  // tables: node list, level descriptors, every next-role node's cost terms
-  // (level 0's `current` is never a next node, and its depth may have no
-  // throughput or cost row)
-  const int first_next = a.levels[0].next_base;
+  // tables, in one pass of independent loads: node list, level descriptors,
+  // per-depth cost terms and the throughput table; then every next-role
+  // node's cost terms from shared memory (level 0's `current` is never a
+  // next node, and its depth may have no throughput or cost row)
+  double4* s_pc = reinterpret_cast<double4*>(sm_raw + G.pc_off());
+  double* s_tt = reinterpret_cast<double*>(sm_raw + G.tt_off());
+  int* s_tr = reinterpret_cast<int*>(sm_raw + G.tr_off());
+  for (int i = threadIdx.x; i < G.n_nodes; i += blockDim.x) s_cfg[i] = a.cfg[i];
+  for (int j = threadIdx.x; j < G.horizon; j += blockDim.x) s_lv[j] = a.levels[j];
+  for (int i = threadIdx.x; i < G.n_pcost; i += blockDim.x) s_pc[i] = a.pcost[i];
+  for (int i = threadIdx.x; i < G.n_thr; i += blockDim.x) s_tt[i] = a.thr_tab[i];
+  for (int i = threadIdx.x; i < G.n_throw; i += blockDim.x) s_tr[i] = a.thr_row[i];
+  __syncthreads();
+  const int first_next = s_lv[0].next_base;
   for (int i = threadIdx.x; i < G.n_nodes; i += blockDim.x) {
-    const NodeCfg nx = a.cfg[i];
-    s_cfg[i] = nx;
+    const NodeCfg nx = s_cfg[i];
     NodeCost nc{0.0, 0.0, 0.0, 0.0};
     if (nx.d > 0 && i >= first_next) {
-      const double4 pc = a.pcost[nx.p];
-      nc.thr = a.thr_tab[a.thr_row[nx.p] + nx.d];
+      const double4 pc = s_pc[nx.p];
+      nc.thr = s_tt[s_tr[nx.p] + nx.d];
       nc.pipe = pc.x;
       nc.unit = pc.y;
       nc.resume = pc.z;
     }
     s_nc[i] = nc;
   }
-  for (int j = threadIdx.x; j < G.horizon; j += blockDim.x) s_lv[j] = a.levels[j];
   if (threadIdx.x == 0) s_vm[0] = make_double2(0.0, 0.0);  // level 0: value 0, migration 0
   // phase 0: probabilities of the fresh entries, split over the cluster
   for (int e = rank; e < a.n_entries; e += kClusterCtas) {
@@ -1006,23 +1028,38 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
     s_base[G.horizon] = b;
   }
   __syncthreads();
-  {  // every prev row the DP reads (L2 reads: written by peer CTAs)
-    const int n_prev = s_lv[G.horizon - 1].next_base;
-    for (int gi = threadIdx.x; gi < n_prev; gi += blockDim.x) {
-      int j = 0;
-      while (j + 1 < G.horizon && s_lv[j + 1].prev_base <= gi) ++j;
-      const LevelDesc& L = s_lv[j];
-      const NodeCfg pv = s_cfg[gi];
-      if (!L.has_hist || pv.d <= 0 || pv.hist_off < 0) continue;
-      const int stride = min(L.k, L.n_now) + 1, len = min(L.k, pv.d) + 1;
-      const double* src = a.store + pv.hist_off;
-      double* dst = s_prob + s_base[j] + (gi - L.prev_base) * stride;
-      for (int d = 0; d < len; ++d) dst[d] = __ldcg(src + d);
+  {  // every prev row the DP reads (L2 reads: written by peer CTAs), one
+     // element per thread so all loads are in flight at once
+    const int n_el = s_base[G.horizon];
+    constexpr int U = 4;
+    for (int e0 = threadIdx.x; e0 < n_el; e0 += U * blockDim.x) {
+      double v[U];
+      int dst[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * blockDim.x;
+        dst[u] = -1;
+        v[u] = 0.0;
+        if (e < n_el) {
+          int j = 0;
+          while (j + 1 < G.horizon && s_base[j + 1] <= e) ++j;
+          const LevelDesc& L = s_lv[j];
+          const int stride = min(L.k, L.n_now) + 1;
+          const int pi = (e - s_base[j]) / stride, d = (e - s_base[j]) - pi * stride;
+          const NodeCfg pv = s_cfg[L.prev_base + pi];
+          dst[u] = e;
+          if (pv.d > 0 && pv.hist_off >= 0 && d <= min(L.k, pv.d)) v[u] = __ldcg(a.store + pv.hist_off + d);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u] >= 0) s_prob[dst[u]] = v[u];
     }
   }
   __syncthreads();
 
   // levels: one warp per next node
+  stamp(1);
   for (int j = 0; j < G.horizon; ++j) {
     const LevelDesc L = s_lv[j];
     const int stride = min(L.k, L.n_now) + 1;
@@ -1035,8 +1072,7 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
       for (int pi = lane; pi < L.prev_count; pi += 32) {
         const int gi = L.prev_base + pi;
         const NodeCfg pv = s_cfg[gi];
-        const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{s_prob + s_base[j] + pi * stride}, a.thr_tab,
-                                  a.thr_row, K);
+        const PhiOut ph = phi_dev(pv, nx, nc, L, S, ProbPtr{s_prob + s_base[j] + pi * stride}, s_tt, s_tr, K);
         const double2 vm = s_vm[gi];
         const double v = __dadd_rn(vm.x, ph.committed);
         const double mg = __dadd_rn(vm.y, ph.mig);
@@ -1068,8 +1104,12 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
         __stcg(a.stm + ni, best.stm);
       }
     }
-    __threadfence();
+    // barrier.cluster arrive.release / wait.acquire orders the DSMEM stores;
+    // the global back-pointers are fenced once, before the last barrier
+    if (j + 1 == G.horizon) __threadfence();
+    stamp(2 + 2 * j);
     cluster.sync();
+    stamp(3 + 2 * j);
   }
 
   // final pick (rank = (value, -mig, D, -P), suspended as (-1, 0), first
@@ -1128,13 +1168,14 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
   }
 }
 
-size_t dp_cluster_smem(int n_nodes, int horizon, int n_prob) {
-  return ClusterLayout{n_nodes, horizon, n_prob}.bytes();
+size_t dp_cluster_smem(int n_nodes, int horizon, int n_prob, int n_pcost, int n_throw, int n_thr) {
+  return ClusterLayout{n_nodes, horizon, n_prob, n_pcost, n_throw, n_thr}.bytes();
 }
 
-cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob) {
+cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob,
+                              int n_pcost, int n_throw, int n_thr) {
   if (a.horizon > kMaxHorizon) return cudaErrorInvalidValue;
-  const ClusterLayout G{n_nodes, a.horizon, n_prob};
+  const ClusterLayout G{n_nodes, a.horizon, n_prob, n_pcost, n_throw, n_thr};
   const size_t smem = G.bytes();
   cudaError_t e = smem_optin(reinterpret_cast<const void*>(dp_cluster_kernel), smem);
   if (e != cudaSuccess) return e;

@@ -112,7 +112,8 @@ size_t dp_staged_smem(int n_nodes, int horizon, int n_prob);
 // Cluster DP (lp_dp.cu): one 8-CTA thread-block cluster, levels separated by
 // barrier.cluster, level values exchanged through distributed shared memory;
 // small re-plans whose whole DP input fits one CTA's shared memory.
-cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob);
-size_t dp_cluster_smem(int n_nodes, int horizon, int n_prob);
+cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars& S, int n_nodes, int n_prob,
+                              int n_pcost, int n_throw, int n_thr);
+size_t dp_cluster_smem(int n_nodes, int horizon, int n_prob, int n_pcost, int n_throw, int n_thr);
 
 }  // namespace lp
