@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kT, (KMAX > 8 ? 3 : 4)) hist_bits_kernel(const
                                                           uint32_t* __restrict__ evt_g,
                                                           uint32_t* __restrict__ h0_g) {
   constexpr int B = KMAX <= 4 ? 2 : (KMAX <= 8 ? 3 : 4);  // bits of KMAX - 1
+  constexpr int TD = KMAX <= 4 ? 2 : 3;  // levels t <= TD emitted after the rows
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x;
   const WorkItem w = work[blockIdx.x];
@@ -145,9 +146,15 @@ __global__ void __launch_bounds__(kT, (KMAX > 8 ? 3 : 4)) hist_bits_kernel(const
 #pragma unroll 1
       for (int g = 0; g < NG; ++g) {
         const uint2* I = info + (ps * NG + g) * 32;
-        uint32_t M[B], J[B];  // running max of R; row of the first collision
+        // J[t-2]: the row at which each depth reached level t (t = 2 .. TD),
+        // emitted after the last row; levels above TD (rare) inline
+        uint32_t M[B], J[TD - 1][B];
 #pragma unroll
-        for (int q = 0; q < B; ++q) M[q] = J[q] = 0u;
+        for (int q = 0; q < B; ++q) {
+          M[q] = 0u;
+#pragma unroll
+          for (int l = 0; l < TD - 1; ++l) J[l][q] = 0u;
+        }
 #pragma unroll
         for (int j = 1; j < KMAX; ++j) {
           if (j >= k) break;
@@ -175,33 +182,45 @@ __global__ void __launch_bounds__(kT, (KMAX > 8 ? 3 : 4)) hist_bits_kernel(const
           }
 #pragma unroll
           for (int q = 0; q < B; ++q) M[q] = (gt & R[q]) | (~gt & M[q]);
-          uint32_t hi = 0u;
+          // an event has R = M_old + 1 = t - 1: record its row per level
+          uint32_t rest = gt;
 #pragma unroll
-          for (int q = 1; q < B; ++q) hi |= R[q];
-          const uint32_t e2 = gt & ~hi;  // first collision: t = 2 at row j
+          for (int l = 0; l < TD - 1; ++l) {
+            uint32_t at = rest;  // R == l + 1
 #pragma unroll
-          for (int q = 0; q < B; ++q)
-            if ((j >> q) & 1) J[q] |= e2;
-          uint32_t e3 = gt & hi;  // t = R + 1 >= 3
-          while (e3) {
-            const int b = __ffs(static_cast<int>(e3)) - 1;
-            e3 &= e3 - 1;
+            for (int q = 0; q < B; ++q) at &= (((l + 1) >> q) & 1) ? R[q] : ~R[q];
+            rest &= ~at;
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+              if ((j >> q) & 1) J[l][q] |= at;
+          }
+          while (rest) {  // t = R + 1 > TD
+            const int b = __ffs(static_cast<int>(rest)) - 1;
+            rest &= rest - 1;
             uint32_t r = 0u;
 #pragma unroll
             for (int q = 0; q < B; ++q) r |= ((R[q] >> b) & 1u) << q;
             emit<SMEM_EVT>(I[b], r - 1u, sj, eb, sink);
           }
         }
-        uint32_t seen = 0u;
+        // depths that reached level t: final M >= t - 1
 #pragma unroll
-        for (int q = 0; q < B; ++q) seen |= M[q];
-        while (seen) {
-          const int b = __ffs(static_cast<int>(seen)) - 1;
-          seen &= seen - 1;
-          uint32_t jj = 0u;
+        for (int l = 0; l < TD - 1; ++l) {
+          uint32_t reached = 0u, eqv = ~0u;  // M > l  (M >= l + 1)
 #pragma unroll
-          for (int q = 0; q < B; ++q) jj |= ((J[q] >> b) & 1u) << q;
-          emit<SMEM_EVT>(I[b], 0u, scol[jj * kT], eb, sink);
+          for (int q = B - 1; q >= 0; --q) {
+            const uint32_t lb = ((l >> q) & 1) ? ~0u : 0u;
+            reached |= eqv & M[q] & ~lb;
+            eqv &= ~(M[q] ^ lb);
+          }
+          while (reached) {
+            const int b = __ffs(static_cast<int>(reached)) - 1;
+            reached &= reached - 1;
+            uint32_t jj = 0u;
+#pragma unroll
+            for (int q = 0; q < B; ++q) jj |= ((J[l][q] >> b) & 1u) << q;
+            emit<SMEM_EVT>(I[b], static_cast<uint32_t>(l), scol[jj * kT], eb, sink);
+          }
         }
       }
     }
