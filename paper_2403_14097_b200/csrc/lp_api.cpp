@@ -371,7 +371,7 @@ const DrawConst& draw_const(uint32_t b) {
       DrawConst d{};
       d.b = v;
       d.lim = UINT64_MAX - UINT64_MAX % v;
-      d.fm = UINT64_MAX / v + 1;
+      d.m32 = v == 1 ? 0xffffffffu : (uint32_t)((1ull << 32) / v);
       d.c32 = (uint32_t)((1ull << 32) % v);
       t[v] = d;
     }

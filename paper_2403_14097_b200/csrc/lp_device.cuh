@@ -2,8 +2,8 @@
 //
 //   * splitmix64 counter streams, bit-exact with the reference Rng
 //     (rng.hpp:11-55): draw i of Rng(s) is fmix64(s + (i+1)*gamma).
-//   * Rng::below without 64-bit division: r % b via three Lemire fastmods of
-//     the 32-bit halves (b < 2^16), rejection limit precomputed per bound.
+//   * Rng::below without 64-bit division: r % b via three Barrett reductions
+//     of the 32-bit halves (b < 2^16), rejection limit precomputed per bound.
 //   * sample_distinct (rng.cpp:8-19) as a sparse partial Fisher-Yates: only
 //     displaced pool positions are recorded, so a trial needs O(k) state
 //     instead of an n-int pool.
@@ -26,22 +26,21 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// Lemire/Kaser/Kurz fastmod: a % d for 32-bit a, d with fm = ceil(2^64 / d).
-// The high product (L * d) >> 64 of L = fm * a mod 2^64 is formed from the
-// 32-bit halves, (hi * d + ((lo * d) >> 32)) >> 32, which is exact: the
-// dropped low word only contributes a fraction below one.
-__device__ __forceinline__ uint32_t fastmod32(uint32_t a, uint64_t fm, uint32_t d) {
-  const uint64_t L = fm * static_cast<uint64_t>(a);
-  const uint32_t lo = static_cast<uint32_t>(L), hi = static_cast<uint32_t>(L >> 32);
-  const uint64_t t = static_cast<uint64_t>(hi) * d + __umulhi(lo, d);
-  return static_cast<uint32_t>(t >> 32);
+// a % d for 32-bit a and d < 2^16 by Barrett reduction with m = floor(2^32 / d)
+// (2^32 - 1 for d = 1): q = umulhi(a, m) is floor(a / d) or one less, so one
+// conditional subtract finishes (exhaustively checked for every d < 2^16,
+// tools/micro/barrett_check.c).  Four instructions.
+__device__ __forceinline__ uint32_t mod32_small(uint32_t a, uint32_t m, uint32_t d) {
+  const uint32_t r = a - __umulhi(a, m) * d;
+  return r >= d ? r - d : r;
 }
 
-// r % b for 64-bit r and b < 2^16: ((hi % b) * (2^32 % b) + lo % b) % b.
+// r % b for 64-bit r and b < 2^16: ((hi % b) * (2^32 % b) + lo % b) % b; the
+// inner sum is below b^2 + b < 2^32.
 __device__ __forceinline__ uint32_t mod64_small(uint64_t r, const DrawConst& c) {
-  const uint32_t hi = fastmod32(static_cast<uint32_t>(r >> 32), c.fm, c.b);
-  const uint32_t lo = fastmod32(static_cast<uint32_t>(r), c.fm, c.b);
-  return fastmod32(hi * c.c32 + lo, c.fm, c.b);
+  const uint32_t hi = mod32_small(static_cast<uint32_t>(r >> 32), c.m32, c.b);
+  const uint32_t lo = mod32_small(static_cast<uint32_t>(r), c.m32, c.b);
+  return mod32_small(hi * c.c32 + lo, c.m32, c.b);
 }
 
 // One Rng::below(b) draw from a splitmix state (rng.hpp:23-30).

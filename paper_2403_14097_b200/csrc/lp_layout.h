@@ -52,7 +52,8 @@ struct EntryDesc {
 // Rng::below(b) for b = n - i (rng.hpp:23-30): reject r >= lim, return r % b.
 struct DrawConst {
   uint64_t lim;         // UINT64_MAX - UINT64_MAX % b
-  uint64_t fm;          // Lemire fastmod multiplier ceil(2^64 / b)
+  uint32_t m32;         // Barrett multiplier floor(2^32 / b) (2^32 - 1 for b = 1)
+  uint32_t pad;
   uint32_t c32;         // 2^32 mod b
   uint32_t b;
 };
