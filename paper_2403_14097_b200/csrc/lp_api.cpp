@@ -567,7 +567,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       }
       continue;
     }
-    if (!legacy && !bits_off && (pd.k <= kIncMaxK || (pd.k <= bits_max_k() && pd.n <= 512))) {
+    if (!legacy && !bits_off && pd.k <= bits_max_k()) {
       // bit-parallel incidence kernel (lp_hist_bits.cu)
       const int km = pd.k <= 4 ? 4 : (pd.k <= 8 ? 8 : 16);
       const size_t kSmemBudgetBits = km > 8 ? kSmemBudgetBits16 : kSmemBudgetBits8;

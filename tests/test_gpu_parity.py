@@ -505,3 +505,20 @@ def test_beyond_2048_instances_vs_oracle(n, k):
         q = planner(w, opt)
         assert plan_rows(q.dp_optimize(cur, ns)) == want
         q.close()
+
+
+@pytest.mark.parametrize("n,k", [(1500, 12), (2048, 16), (700, 9)])
+def test_large_n_mid_k_vs_oracle(n, k):
+    """512 < n <= 2048 with 9 <= k <= 16 runs the bits kernel (round 1 used the
+    first-generation dense kernel here): counts of sampled configs against the
+    oracle."""
+    w = resnet152_dp()
+    trials = 3000
+    p = planner(w, PlannerOptions(mc_trials=trials, exact_cap=0))
+    cs = O.oracle_configs(w, n)
+    sel = cs[:: max(1, len(cs) // 16)] + [ParallelConfig(n, 1), ParallelConfig(n // 2, 2)]
+    ref, tot = O.oracle_ensemble_counts(n, k, False, trials, O.planner_seed(0x5EED, n, k), sel)
+    for ci, c in enumerate(sel):
+        got, gt = p.survivor_counts(c, n, k)
+        assert gt == tot and got.tolist() == ref[ci][: c.pipelines + 1].tolist(), (n, k, c)
+    p.close()
