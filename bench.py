@@ -182,6 +182,17 @@ class RefArm:
                 f"instead of the workload's trial count, {self.threads} threads")
 
 
+def load_int_peak():
+    """Measured integer pipe rates (tools/micro/int_peak.cu on a B200)."""
+    p = ROOT / "profiles" / "int_peak.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
 def load_profile_issue():
     """Issue-slot utilisation of the dominant kernel from the committed ncu
     capture (sm__inst_issued / (SM cycles x 4 schedulers))."""
@@ -417,7 +428,10 @@ def main():
     clocks = clk.summary()
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-    peak_gops = n_sm * 4 * 32 * sm_mhz * 1e6 / 1e9
+    issue_peak_gops = n_sm * 4 * 32 * sm_mhz * 1e6 / 1e9
+    ipk = load_int_peak()
+    alu_per_sm = (ipk or {}).get("alu_lane_ops_per_cycle_per_sm", 64.0)
+    peak_gops = n_sm * alu_per_sm * sm_mhz * 1e6 / 1e9  # the measured ALU-pipe peak (LOP3)
     hist_med = statistics.median(hist_ms)
     achieved_gops = st.hist_alg_ops / (hist_med / 1e3) / 1e9
     survey_gops = st.hist_survey_ops / (hist_med / 1e3) / 1e9
@@ -439,17 +453,20 @@ def main():
         "gpu_launches": st.kernel_launches * args.steps,
         "e2e": {"value": e2e_value, "unit": "resolutions/s", "ms_per_step": e2e_s * 1e3 / args.steps,
                 "h2d_bytes_per_step": int(st2.h2d_bytes), "d2h_bytes_per_step": int(st2.d2h_bytes)},
-        "roofline": {"bound": "int-issue", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
+        "roofline": {"bound": "int-alu", "achieved": achieved_gops, "peak": peak_gops, "unit": "Gop/s",
                      "frac": achieved_gops / peak_gops, "frac_model": achieved_gops / peak_gops,
+                     "peak_issue": issue_peak_gops, "frac_issue_model": achieved_gops / issue_peak_gops,
                      "model": "int32 ops of the algorithms as run (DESIGN.md §5.2): generation 20+35k per "
                               "scenario; bits kernel k(k-1)/2 x (2B+1) + (k-1) x (5B+3) per 32-depth group; "
                               "row kernel Dmax x ceil(P/32) x (3B+4) per depth; events not counted",
-                     "frac_survey_model": survey_gops / peak_gops,
+                     "frac_survey_model": survey_gops / issue_peak_gops,
                      "survey_ops_per_step": st.hist_survey_ops,
                      "issue_frac": issue.get("issue_frac") if issue else None,
+                     "alu_pipe_busy": issue.get("alu_pipe_busy") if issue else None,
                      "issue_source": issue.get("source") if issue else None,
-                     "peak_source": f"{n_sm} SM x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz measured SM clock "
-                                    "(1 int32 lane-op/lane/cycle issue)",
+                     "peak_source": f"{n_sm} SM x {alu_per_sm} ALU-pipe lane-ops/cycle (LOP3, measured by "
+                                    f"tools/micro/int_peak.cu, profiles/int_peak.json) x {sm_mhz:.0f} MHz measured SM "
+                                    "clock; peak_issue = 4 SMSP x 32 lanes per cycle",
                      "kernel": "hist_* (K1: scenario generation + threshold-event resolution), incl. finalize",
                      "alg_ops_per_step": st.hist_alg_ops,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None},
