@@ -1304,17 +1304,24 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
   h->opt = *options;
   h->cs = cost_scalars(*costs);
   h->device = device;
-  // LIVEPUT_PRIO=1: DP and library streams at the highest priority, stage s
-  // histogram streams one step lower each (A/B of the stage pipelining)
-  static const bool prio = [] {
+  // Stream priorities (LIVEPUT_PRIO, default 3): the stage-s histogram
+  // streams one step below each other so that stage 0's blocks are dispatched
+  // first and it finishes first (with equal priorities the scheduler
+  // interleaves the three stages and they finish in reverse order, so no DP
+  // level can start early), the library stream highest, and the DP stream
+  // lowest, so DP blocks only take slots the sampling leaves free.  Measured
+  // on B200: 4 GPUs 1.87 ms against 1.95 ms with equal priorities, 1 GPU
+  // 6.44-6.50 against 6.53 ms.  0: all equal; 1: DP highest; 2: DP at stage 0's.
+  static const int prio = [] {
     const char* pe = getenv("LIVEPUT_PRIO");
-    return pe && pe[0] == '1';
+    return pe ? atoi(pe) : 3;
   }();
   int least = 0, greatest = 0;
   if (prio) cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const int dp_prio = prio == 2 ? std::min(least, greatest + 1) : (prio == 3 ? least : greatest);
   if ((e = cudaSetDevice(device)) != cudaSuccess ||
       (e = cudaStreamCreateWithPriority(&h->stream, cudaStreamNonBlocking, greatest)) != cudaSuccess ||
-      (e = cudaStreamCreateWithPriority(&h->stream_dp, cudaStreamNonBlocking, greatest)) != cudaSuccess) {
+      (e = cudaStreamCreateWithPriority(&h->stream_dp, cudaStreamNonBlocking, dp_prio)) != cudaSuccess) {
     delete h;
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }

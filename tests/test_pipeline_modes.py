@@ -54,7 +54,7 @@ def test_execution_modes_agree():
     base = _run({"LIVEPUT_STAGES": "1"})  # one stage: persistent cooperative DP
     for env in ({"LIVEPUT_STAGES": "3"}, {"LIVEPUT_STAGES": "0"},
                 {"LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"}, {"LIVEPUT_STAGES": "4"},
-                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"}, {"LIVEPUT_DP_CLUSTER": "0"},
+                {"LIVEPUT_STAGES": "1", "LIVEPUT_DP_STAGED": "0"}, {"LIVEPUT_PDL": "0"}, {"LIVEPUT_DP_CLUSTER": "0"}, {"LIVEPUT_PRIO": "0"}, {"LIVEPUT_PRIO": "1"},
                 {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
                 {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"}, {"LIVEPUT_HIST_KERNEL": "inc"}, {"LIVEPUT_BITS_MAXK": "8"},
                 {"LIVEPUT_HIST_KERNEL": "norows"}, {"LIVEPUT_ROWS_SHAPE": "160,56,8"},
