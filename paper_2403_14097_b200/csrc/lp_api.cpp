@@ -481,11 +481,12 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   mark("pairs");
   // scenarios per block: enough blocks for ~24 per SM over all ensembles
   // (short blocks keep the last wave short; trial-sharded ranks keep every SM
-  // busy), at most 8 per thread (measured: 2048 beats 4096 by 2% at N = 256)
+  // busy), at most 4 per 256-thread block (measured with the prioritised stage
+  // streams, bench re-plan: 1024 6.32-6.35 ms, 1536 6.38, 2048 6.49)
   uint64_t local_total = 0;
   for (const PairDesc& pd : hp.pairs) local_total += pd.t_hi - pd.t_lo;
   const uint64_t want_blocks = (uint64_t)std::max(num_sms, 1) * 24;
-  uint64_t per_block = std::min<uint64_t>(2048, std::max<uint64_t>(256, ((local_total / want_blocks) + 255) & ~255ull));
+  uint64_t per_block = std::min<uint64_t>(1024, std::max<uint64_t>(256, ((local_total / want_blocks) + 255) & ~255ull));
   if (const char* pb = getenv("LIVEPUT_PER_BLOCK")) per_block = std::max<uint64_t>(256, strtoull(pb, nullptr, 10));
 
   // work items, grouped by launch configuration
