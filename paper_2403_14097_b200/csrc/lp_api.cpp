@@ -1021,7 +1021,9 @@ struct lp_handle {
   DpScalars S{};
   size_t off_divtab = 0, off_dmask = 0;
   size_t off_pairs = 0, off_entries = 0, off_draws = 0, off_binom = 0, off_work = 0,
-         off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0;
+         off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0,
+         off_gather = 0, off_pbase = 0;
+  std::vector<int32_t> dp_gather, dp_pbase;  // cluster DP staging lists
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
          w_plan = 0, w_live = 0, w_final = 0, w_bar = 0;
   int max_next = 0;         // largest level (next role), for the persistent DP grid
@@ -1872,11 +1874,36 @@ lp_status prepare_dp(lp_handle* h) {
                     dp_cluster_smem(n_nodes, H, (int)nprob, (int)h->pcost.size(), (int)h->thr.row.size(),
                                     (int)h->thr.vals.size()) <= 200 * 1024;
   }
+  // cluster DP: the staged probability layout is built here, so the kernel
+  // gathers its rows in one pass of independent loads
+  h->dp_gather.clear();
+  h->dp_pbase.clear();
+  if (h->dp_cluster) {
+    h->dp_gather.assign(std::max(h->dp_staged_nprob, 1), -1);
+    h->dp_pbase.assign(H + 1, 0);
+    int b = 0;
+    for (int j = 0; j < H; ++j) {
+      h->dp_pbase[j] = b;
+      const LevelDesc& L = h->levels[j];
+      if (!L.has_hist) continue;
+      const int stride = std::min(L.k, L.n_now) + 1;
+      for (int i = 0; i < L.prev_count; ++i) {
+        const NodeCfg& c = h->cfg[L.prev_base + i];
+        if (c.d > 0 && c.hist_off >= 0) {
+          const int len = std::min(L.k, c.d) + 1;
+          for (int d = 0; d < len; ++d) h->dp_gather[b + i * stride + d] = c.hist_off + d;
+        }
+      }
+      b += L.prev_count * stride;
+    }
+    h->dp_pbase[H] = b;
+  }
   size_t bytes = 0;
   lp_status us = upload_image(h,
                               {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
                                sec(h->pcost, &h->off_cost), sec(h->lrows, &h->off_lrows),
-                               sec(h->thr.vals, &h->off_thr), sec(h->thr.row, &h->off_throw)},
+                               sec(h->thr.vals, &h->off_thr), sec(h->thr.row, &h->off_throw),
+                               sec(h->dp_gather, &h->off_gather), sec(h->dp_pbase, &h->off_pbase)},
                               h->tables2, h->pin_up2, h->ev_up[1], &bytes, h->stream_dp);
   if (us != LP_OK) return us;
   mark("upload2");
@@ -2000,6 +2027,8 @@ lp_status exec_dp(lp_handle* h) {
     a.barrier = dptr<uint32_t>(h->work, h->w_bar);
     a.horizon = h->horizon;
     a.max_next = std::max(1, h->max_next);
+    a.gather = h->dp_cluster ? dptr<int32_t>(h->tables2, h->off_gather) : nullptr;
+    a.pbase = h->dp_cluster ? dptr<int32_t>(h->tables2, h->off_pbase) : nullptr;
     static const bool trace = getenv("LIVEPUT_DP_TRACE") != nullptr;
     if (trace) {
       const size_t nb = (size_t)h->num_sms * 8 * (2 * kTraceLevels + 2);

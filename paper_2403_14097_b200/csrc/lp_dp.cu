@@ -984,6 +984,17 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
   double4* s_pc = reinterpret_cast<double4*>(sm_raw + G.pc_off());
   double* s_tt = reinterpret_cast<double*>(sm_raw + G.tt_off());
   int* s_tr = reinterpret_cast<int*>(sm_raw + G.tr_off());
+  // every prev row the DP reads, gathered by the host-built offset list in
+  // the same pass of independent loads when no histogram of this re-plan is
+  // fresh (a warm re-plan), else after the normalisation below
+  auto stage_rows = [&]() {
+    for (int e = threadIdx.x; e < G.n_prob; e += blockDim.x) {
+      const int src = a.gather[e];
+      s_prob[e] = src >= 0 ? __ldcg(a.store + src) : 0.0;
+    }
+  };
+  if (a.n_entries == 0) stage_rows();
+  for (int j = threadIdx.x; j <= G.horizon; j += blockDim.x) s_base[j] = a.pbase[j];
   for (int i = threadIdx.x; i < G.n_nodes; i += blockDim.x) s_cfg[i] = a.cfg[i];
   for (int j = threadIdx.x; j < G.horizon; j += blockDim.x) s_lv[j] = a.levels[j];
   for (int i = threadIdx.x; i < G.n_pcost; i += blockDim.x) s_pc[i] = a.pcost[i];
@@ -1016,47 +1027,14 @@ __global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterT
       out[i] = c ? __ddiv_rn(static_cast<double>(c), total) : 0.0;
     }
   }
-  __threadfence();
-  cluster.sync();  // the store is complete (every CTA's normalisation)
-  if (threadIdx.x == 0) {
-    int b = 0;
-    for (int j = 0; j < G.horizon; ++j) {
-      s_base[j] = b;
-      const LevelDesc& L = s_lv[j];
-      if (L.has_hist) b += L.prev_count * (min(L.k, L.n_now) + 1);
-    }
-    s_base[G.horizon] = b;
+  if (a.n_entries > 0) {
+    __threadfence();
+    cluster.sync();  // the store is complete (every CTA's normalisation)
+    stage_rows();
+    __syncthreads();
+  } else {
+    cluster.sync();  // every CTA runs before any DSMEM store reaches it
   }
-  __syncthreads();
-  {  // every prev row the DP reads (L2 reads: written by peer CTAs), one
-     // element per thread so all loads are in flight at once
-    const int n_el = s_base[G.horizon];
-    constexpr int U = 4;
-    for (int e0 = threadIdx.x; e0 < n_el; e0 += U * blockDim.x) {
-      double v[U];
-      int dst[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * blockDim.x;
-        dst[u] = -1;
-        v[u] = 0.0;
-        if (e < n_el) {
-          int j = 0;
-          while (j + 1 < G.horizon && s_base[j + 1] <= e) ++j;
-          const LevelDesc& L = s_lv[j];
-          const int stride = min(L.k, L.n_now) + 1;
-          const int pi = (e - s_base[j]) / stride, d = (e - s_base[j]) - pi * stride;
-          const NodeCfg pv = s_cfg[L.prev_base + pi];
-          dst[u] = e;
-          if (pv.d > 0 && pv.hist_off >= 0 && d <= min(L.k, pv.d)) v[u] = __ldcg(a.store + pv.hist_off + d);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (dst[u] >= 0) s_prob[dst[u]] = v[u];
-    }
-  }
-  __syncthreads();
 
   // levels: one warp per next node
   stamp(1);

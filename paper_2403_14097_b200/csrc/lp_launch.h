@@ -100,6 +100,10 @@ struct DpArgs {
   int horizon;
   int max_next;     // largest next-level node count: the blocks that run the levels
   uint64_t* trace;  // optional: per block, 2 * kTraceLevels + 2 globaltimer stamps
+  // cluster DP: per staged probability element its store offset (-1: +0.0),
+  // and each level's first element (horizon + 1), both built on the host
+  const int32_t* gather;
+  const int32_t* pbase;
 };
 constexpr int kTraceLevels = 32;
 
