@@ -186,3 +186,22 @@ def test_live_dp_n96():
     a = O.RefPlanner(w, CostTable(), opt).dp_optimize(cur, ns)
     b = O.OraclePlanner(w, CostTable(), opt).dp_optimize(cur, ns)
     assert a == b
+
+
+def test_oracle_memo_identical():
+    """The restatement's opt-in per-(n, k) memo (used to generate the long 1e6
+    replay fixtures) gives the same plans and values as the cache-free path."""
+    import json
+    from pathlib import Path
+    from oracle.oracle import OraclePlanner
+    from paper_2403_14097_b200.model import CostTable, ParallelConfig, PlannerOptions, lm_6p7b
+    counts = json.loads((Path(__file__).resolve().parents[1] / "tools" / "data" /
+                         "trace_gen_synthetic_128.json").read_text())["counts"]
+    w = lm_6p7b()
+    opt = PlannerOptions(mc_trials=3000)
+    a = OraclePlanner(w, CostTable(), opt, cache=True)
+    b = OraclePlanner(w, CostTable(), opt)
+    cur = ParallelConfig(4, 20)
+    for i in range(0, 60, 6):
+        ns = counts[i:i + 13]
+        assert a.dp_optimize(cur, ns) == b.dp_optimize(cur, ns), i
