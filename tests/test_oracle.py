@@ -201,7 +201,7 @@ def test_oracle_memo_identical():
     opt = PlannerOptions(mc_trials=3000)
     a = OraclePlanner(w, CostTable(), opt, cache=True)
     b = OraclePlanner(w, CostTable(), opt)
-    cur = ParallelConfig(4, 20)
+    cur = ParallelConfig(3, 20)  # fits every count of the first 60 intervals (>= 66)
     for i in range(0, 60, 6):
         ns = counts[i:i + 13]
         assert a.dp_optimize(cur, ns) == b.dp_optimize(cur, ns), i
