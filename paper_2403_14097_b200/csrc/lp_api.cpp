@@ -373,6 +373,7 @@ const DrawConst& draw_const(uint32_t b) {
       d.lim = UINT64_MAX - UINT64_MAX % v;
       d.m32 = v == 1 ? 0xffffffffu : (uint32_t)((1ull << 32) / v);
       d.c32 = (uint32_t)((1ull << 32) % v);
+      d.negb = 0u - v;
       t[v] = d;
     }
     return t;

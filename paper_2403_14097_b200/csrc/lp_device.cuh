@@ -2,8 +2,9 @@
 //
 //   * splitmix64 counter streams, bit-exact with the reference Rng
 //     (rng.hpp:11-55): draw i of Rng(s) is fmix64(s + (i+1)*gamma).
-//   * Rng::below without 64-bit division: r % b via three Barrett reductions
-//     of the 32-bit halves (b < 2^16), rejection limit precomputed per bound.
+//   * Rng::below without 64-bit division: r % b via three lazy Barrett
+//     reductions of the 32-bit halves (b <= kMaxN), rejection limit
+//     precomputed per bound.
 //   * sample_distinct (rng.cpp:8-19) as a sparse partial Fisher-Yates: only
 //     displaced pool positions are recorded, so a trial needs O(k) state
 //     instead of an n-int pool.
@@ -26,21 +27,23 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// a % d for 32-bit a and d < 2^16 by Barrett reduction with m = floor(2^32 / d)
-// (2^32 - 1 for d = 1): q = umulhi(a, m) is floor(a / d) or one less, so one
-// conditional subtract finishes (exhaustively checked for every d < 2^16,
-// tools/micro/barrett_check.c).  Four instructions.
-__device__ __forceinline__ uint32_t mod32_small(uint32_t a, uint32_t m, uint32_t d) {
-  const uint32_t r = a - __umulhi(a, m) * d;
-  return r >= d ? r - d : r;
+// Lazy Barrett reduction with m = floor(2^32 / d) (2^32 - 1 for d = 1):
+// q = umulhi(a, m) is floor(a / d) or one less, so a - q d is congruent to a
+// mod d and lies in [0, 2d).  negd = 2^32 - d makes it one IMAD after the
+// IMAD.HI.
+__device__ __forceinline__ uint32_t mod32_lazy(uint32_t a, uint32_t m, uint32_t negd) {
+  return a + __umulhi(a, m) * negd;
 }
 
-// r % b for 64-bit r and b < 2^16: ((hi % b) * (2^32 % b) + lo % b) % b; the
-// inner sum is below b^2 + b < 2^32.
+// r % b for 64-bit r and b <= kMaxN: the halves are reduced lazily to [0, 2b),
+// so h (2^32 mod b) + l < 2b(b + 1) < 2^32 for b < 46341; one more lazy
+// reduction and min(x, x - b) (unsigned: x - b wraps when x < b) finish.
+// Nine instructions (tools/micro/barrett_check.c checks b <= 46340).
 __device__ __forceinline__ uint32_t mod64_small(uint64_t r, const DrawConst& c) {
-  const uint32_t hi = mod32_small(static_cast<uint32_t>(r >> 32), c.m32, c.b);
-  const uint32_t lo = mod32_small(static_cast<uint32_t>(r), c.m32, c.b);
-  return mod32_small(hi * c.c32 + lo, c.m32, c.b);
+  const uint32_t h = mod32_lazy(static_cast<uint32_t>(r >> 32), c.m32, c.negb);
+  const uint32_t l = mod32_lazy(static_cast<uint32_t>(r), c.m32, c.negb);
+  const uint32_t x = mod32_lazy(h * c.c32 + l, c.m32, c.negb);
+  return min(x, x + c.negb);
 }
 
 // One Rng::below(b) draw from a splitmix state (rng.hpp:23-30).

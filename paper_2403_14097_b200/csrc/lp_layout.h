@@ -53,7 +53,7 @@ struct EntryDesc {
 struct DrawConst {
   uint64_t lim;         // UINT64_MAX - UINT64_MAX % b
   uint32_t m32;         // Barrett multiplier floor(2^32 / b) (2^32 - 1 for b = 1)
-  uint32_t pad;
+  uint32_t negb;        // 2^32 - b
   uint32_t c32;         // 2^32 mod b
   uint32_t b;
 };
