@@ -999,6 +999,17 @@ struct lp_handle {
   cudaEvent_t ev_hist[kMaxStages] = {};       // ... done
   cudaEvent_t ev_start = nullptr;             // scratch cleared for this execute
   cudaEvent_t ev_join = nullptr;
+  // materialised phi (pipelined re-plans): the phi launches of stage s run on
+  // their own stream and release the max-plus levels with ev_phi[s]
+  cudaStream_t stream_phi = nullptr;
+  cudaEvent_t ev_phi[kMaxStages] = {};
+  std::vector<cudaEvent_t> ev_lvl;        // last stage: phi of level j done
+  bool phi_on = false;
+  DevBuf phi;
+  std::vector<int32_t> phi_list;          // levels ordered by the stage that releases them
+  std::vector<int> phi_range;             // per stage: [phi_range[s], phi_range[s+1]) of phi_list
+  std::vector<int64_t> phi_maxpairs;      // per stage: largest prev count (the phi grid)
+  size_t off_phi_list = 0;
   std::vector<cudaEvent_t> tl_ev;  // LIVEPUT_TIMELINE: one event per DP level (diagnostics)
   std::vector<int> level_need;  // per DP level: the last stage it must wait for (-1: none)
   std::string err;
@@ -1339,6 +1350,17 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
                                  prio ? std::min(least, greatest + 1 + q) : 0);
   cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+  for (auto& ev : h->ev_phi) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  {
+    // LIVEPUT_PHI_PRIO: phi launches at the highest priority (default), 1:
+    // at stage 0's, 2: the lowest (A/B)
+    static const int pp = [] {
+      const char* e = getenv("LIVEPUT_PHI_PRIO");
+      return e ? atoi(e) : 0;
+    }();
+    const int phi_prio = pp == 1 ? std::min(least, greatest + 1) : (pp == 2 ? least : greatest);
+    cudaStreamCreateWithPriority(&h->stream_phi, cudaStreamNonBlocking, phi_prio);
+  }
   {
     const char* e = getenv("LIVEPUT_DP");
     h->dp_launches = (e && std::string(e) == "launches");
@@ -1372,6 +1394,13 @@ void lp_destroy(lp_handle* h) {
     }
   if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  for (auto& ev : h->ev_phi)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : h->ev_lvl) cudaEventDestroy(ev);
+  if (h->stream_phi) {
+    cudaStreamSynchronize(h->stream_phi);
+    cudaStreamDestroy(h->stream_phi);
+  }
   if (h->stream_dp) {
     cudaStreamSynchronize(h->stream_dp);
     cudaStreamDestroy(h->stream_dp);
@@ -1899,12 +1928,65 @@ lp_status prepare_dp(lp_handle* h) {
     }
     h->dp_pbase[H] = b;
   }
+  // Materialised phi (LIVEPUT_PHI, off by default): a pipelined re-plan
+  // evaluates level j's pairs in the phi launch of the stage that releases
+  // it, so the level chain left after the sampling is max-plus passes only.
+  // Measured on B200 (bench re-plan): on one GPU -5.5% at
+  // 125K samples per ensemble and -1.6% at 250K, +0.7% at 1e6; under
+  // torchrun on 4 GPUs +1.3% (1.91 against 1.89 ms), so it stays an A/B
+  // path.  LIVEPUT_PHI=1: every pipelined re-plan; LIVEPUT_PHI=<n> > 1: those
+  // whose per-rank ensemble share is at most n samples.  LIVEPUT_PHI_MAX_MB
+  // bounds the phi buffer (default 1024).
+  {
+    static const int64_t phi_max = [] {
+      const char* e = getenv("LIVEPUT_PHI_MAX_MB");
+      return (e ? atoll(e) : 1024LL) << 20;
+    }();
+    static const uint64_t phi_trials = [] {  // 0: off, UINT64_MAX: always
+      const char* e = getenv("LIVEPUT_PHI");
+      const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0ull;
+      return v == 1 ? UINT64_MAX : (uint64_t)v;
+    }();
+    const int nst = (int)h->hp.stages.size();
+    const bool persistent = nst <= 1 && !h->dp_launches && H <= kMaxHorizon;
+    uint64_t local = 0;
+    for (const PairDesc& pd : h->hp.pairs) local = std::max<uint64_t>(local, pd.t_hi - pd.t_lo);
+    int64_t pairs = 0;
+    for (int j = 0; j < H; ++j) pairs += (int64_t)h->levels[j].prev_count * h->levels[j].next_count;
+    h->phi_on = !persistent && local <= phi_trials && pairs > 0 && pairs * 16 <= phi_max &&
+                pairs < (int64_t(1) << 31);
+    h->phi_list.clear();
+    const int ns = std::max(nst, 1);
+    h->phi_range.assign(ns + 1, 0);
+    h->phi_maxpairs.assign(ns, 0);
+    if (h->phi_on) {
+      int64_t o = 0;
+      std::vector<std::vector<int32_t>> by_stage(ns);
+      for (int j = 0; j < H; ++j) {
+        LevelDesc& L = h->levels[j];
+        L.phi_off = (int32_t)o;
+        const int64_t np = (int64_t)L.prev_count * L.next_count;
+        o += np;
+        if (np == 0) continue;
+        const int s = j < (int)h->level_need.size() ? std::max(0, std::min(h->level_need[j], ns - 1)) : ns - 1;
+        by_stage[s].push_back(j);
+        h->phi_maxpairs[s] = std::max<int64_t>(h->phi_maxpairs[s], L.prev_count);
+      }
+      for (int s = 0; s < ns; ++s) {
+        h->phi_range[s] = (int)h->phi_list.size();
+        h->phi_list.insert(h->phi_list.end(), by_stage[s].begin(), by_stage[s].end());
+      }
+      h->phi_range[ns] = (int)h->phi_list.size();
+      LP_CUDA(h, h->phi.ensure((size_t)o * 16));
+    }
+  }
   size_t bytes = 0;
   lp_status us = upload_image(h,
                               {sec(h->levels, &h->off_levels), sec(h->cfg, &h->off_cfg),
                                sec(h->pcost, &h->off_cost), sec(h->lrows, &h->off_lrows),
                                sec(h->thr.vals, &h->off_thr), sec(h->thr.row, &h->off_throw),
-                               sec(h->dp_gather, &h->off_gather), sec(h->dp_pbase, &h->off_pbase)},
+                               sec(h->dp_gather, &h->off_gather), sec(h->dp_pbase, &h->off_pbase),
+                               sec(h->phi_list, &h->off_phi_list)},
                               h->tables2, h->pin_up2, h->ev_up[1], &bytes, h->stream_dp);
   if (us != LP_OK) return us;
   mark("upload2");
@@ -2048,35 +2130,114 @@ lp_status exec_dp(lp_handle* h) {
   } else {
     LP_CUDA(h, cudaMemsetAsync(val, 0, 8, st));  // level 0: value 0, migration 0
     LP_CUDA(h, cudaMemsetAsync(mig, 0, 8, st));
-    int waited = -1;
-    static const bool pdl_on = [] {  // LIVEPUT_PDL=0: plain stream order between levels (A/B)
-      const char* e = getenv("LIVEPUT_PDL");
-      return !(e && e[0] == '0');
-    }();
-    for (int j = 0; j < h->horizon; ++j) {
-      const int need = j < (int)h->level_need.size() ? h->level_need[j] : nst - 1;
-      bool pdl = pdl_on && j > 0;  // right after a cross-stream wait: plain order
-      if (need > waited) {
-        LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[need], 0));
-        waited = need;
-        pdl = false;
+    if (h->phi_on) {
+      // phi of the levels each stage releases, on the phi stream (highest
+      // priority), as soon as that stage's probabilities are in the store
+      double2* phi = static_cast<double2*>(h->phi.p);
+      const int32_t* lv_list = dptr<int32_t>(h->tables2, h->off_phi_list);
+      const int ns = (int)h->phi_maxpairs.size();
+      LP_CUDA(h, cudaStreamWaitEvent(h->stream_phi, h->ev_up[1], 0));  // the DP image
+      // one phi launch per stage, except that the last stage's levels get a
+      // launch and an event each, so the chain left after the sampling starts
+      // on its first level's pairs.  LIVEPUT_PHI_LEVELS=1: per-level launches
+      // and events for every stage (measured slower: a cross-stream wait per
+      // level costs more than the earlier start saves)
+      static const bool phi_per_level = [] {
+        const char* e = getenv("LIVEPUT_PHI_LEVELS");
+        return e && e[0] == '1';
+      }();
+      while ((int)h->ev_lvl.size() < h->horizon) {
+        cudaEvent_t e;
+        LP_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->ev_lvl.push_back(e);
       }
-      LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, pdl, st, lv, cfg, pcost,
-                                histp, thr, throw_, h->S, val, mig, par, stc, stm));
-      ++launches;
-      if (timeline()) {
-        while ((int)h->tl_ev.size() <= j) {
-          cudaEvent_t e;
-          LP_CUDA(h, cudaEventCreate(&e));
-          h->tl_ev.push_back(e);
+      for (int s = 0; s < ns; ++s) {
+        if (s < nst) LP_CUDA(h, cudaStreamWaitEvent(h->stream_phi, h->ev_stage[s], 0));
+        const int a = h->phi_range[s], b = h->phi_range[s + 1];
+        if (!phi_per_level && s < ns - 1) {
+          LP_CUDA(h, launch_phi_matrix(b - a, h->phi_maxpairs[s], h->stream_phi, lv_list + a, lv, cfg, pcost, histp,
+                                       thr, throw_, h->S, phi));
+          if (b > a) ++launches;
+          LP_CUDA(h, cudaEventRecord(h->ev_phi[s], h->stream_phi));
+          continue;
         }
-        LP_CUDA(h, cudaEventRecord(h->tl_ev[j], st));
+        for (int q = a; q < b; ++q) {
+          const int j = h->phi_list[q];
+          LP_CUDA(h, launch_phi_matrix(1, h->levels[j].prev_count, h->stream_phi, lv_list + q, lv, cfg, pcost, histp,
+                                       thr, throw_, h->S, phi));
+          ++launches;
+          LP_CUDA(h, cudaEventRecord(h->ev_lvl[j], h->stream_phi));
+        }
+        LP_CUDA(h, cudaEventRecord(h->ev_phi[s], h->stream_phi));
       }
+      static const bool pdl_on = [] {
+        const char* e = getenv("LIVEPUT_PDL");
+        return !(e && e[0] == '0');
+      }();
+      // the max-plus levels, PDL-chained while they follow a stage event;
+      // the last stage's levels each wait for their own phi launch
+      int waited = -1;
+      for (int j = 0; j < h->horizon; ++j) {
+        int need = j < (int)h->level_need.size() ? h->level_need[j] : ns - 1;
+        need = std::max(0, std::min(need, ns - 1));
+        bool pdl = pdl_on && j > 0;
+        if ((phi_per_level || need == ns - 1) && h->levels[j].prev_count > 0 && h->levels[j].next_count > 0) {
+          LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_lvl[j], 0));
+          pdl = false;
+        } else if (need > waited) {
+          LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_phi[need], 0));
+          waited = need;
+          pdl = false;
+        }
+        LP_CUDA(h, launch_dp_maxplus(j, h->levels[j].next_count, pdl, st, lv, phi, val, mig, par, stc, stm));
+        ++launches;
+        if (timeline()) {
+          while ((int)h->tl_ev.size() <= j) {
+            cudaEvent_t e;
+            LP_CUDA(h, cudaEventCreate(&e));
+            h->tl_ev.push_back(e);
+          }
+          LP_CUDA(h, cudaEventRecord(h->tl_ev[j], st));
+        }
+      }
+      LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_phi[ns - 1], 0));
+      const LevelDesc& last = h->levels[h->horizon - 1];
+      LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
+                                 dptr<lp_plan_step>(h->work, h->w_plan), dptr<double>(h->work, h->w_final),
+                                 last.next_base + last.next_count));
+      ++launches;
+    } else {
+      int waited = -1;
+      static const bool pdl_on = [] {  // LIVEPUT_PDL=0: plain stream order between levels (A/B)
+        const char* e = getenv("LIVEPUT_PDL");
+        return !(e && e[0] == '0');
+      }();
+      for (int j = 0; j < h->horizon; ++j) {
+        const int need = j < (int)h->level_need.size() ? h->level_need[j] : nst - 1;
+        bool pdl = pdl_on && j > 0;  // right after a cross-stream wait: plain order
+        if (need > waited) {
+          LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[need], 0));
+          waited = need;
+          pdl = false;
+        }
+        LP_CUDA(h, launch_dp_step(j, h->levels[j].next_count, h->levels[j].prev_count, pdl, st, lv, cfg, pcost,
+                                  histp, thr, throw_, h->S, val, mig, par, stc, stm));
+        ++launches;
+        if (timeline()) {
+          while ((int)h->tl_ev.size() <= j) {
+            cudaEvent_t e;
+            LP_CUDA(h, cudaEventCreate(&e));
+            h->tl_ev.push_back(e);
+          }
+          LP_CUDA(h, cudaEventRecord(h->tl_ev[j], st));
+        }
+      }
+      const LevelDesc& last = h->levels[h->horizon - 1];
+      LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
+                                 dptr<lp_plan_step>(h->work, h->w_plan), dptr<double>(h->work, h->w_final),
+                                 last.next_base + last.next_count));
+      ++launches;
     }
-    LP_CUDA(h, launch_dp_final(h->horizon, st, lv, cfg, val, mig, par, stc, stm,
-                               dptr<lp_plan_step>(h->work, h->w_plan),
-                               dptr<double>(h->work, h->w_final)));
-    ++launches;
   }
   // every stage has landed in the store before the handle's stream moves on
   if (nst > 0) LP_CUDA(h, cudaStreamWaitEvent(st, h->ev_stage[nst - 1], 0));

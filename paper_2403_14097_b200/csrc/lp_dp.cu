@@ -418,28 +418,211 @@ __global__ void __launch_bounds__(512) dp_step_kernel(int j, const LevelDesc* __
   }
 }
 
+// Materialised phi for the pipelined re-plan.  phi(prev, next) of level j
+// depends only on the level's histograms and the two configs, never on the
+// DP values, so it is taken off the level chain: once a pipeline stage's
+// probabilities are in the store, throughput launches evaluate every
+// (prev, next) pair of the levels that stage released into
+// phi[L.phi_off + prev * next_count + next] = (committed, mig).
+// One block per (level, kPhiG consecutive prevs): each prev's nonzero bins
+// are compacted in shared memory in summation order (d = dmax .. 0, i.e.
+// m ascending); each thread then takes next nodes, loads the next node's
+// constants once and sums the kPhiG prevs against them.  Skipping a zero bin
+// is exact (it adds +0.0 to non-negative sums), and every other operation
+// is phi_dev's, in its order, so the values are phi_dev's bit for bit.
+// blockIdx.y indexes the launch's level list.
+constexpr int kPhiG = 4;        // prevs per block
+constexpr int kPhiBins = 512;   // longer rows take phi_dev on the store directly
+
+__global__ void __launch_bounds__(256) phi_matrix_kernel(const int32_t* __restrict__ lv_list,
+                                                         const LevelDesc* __restrict__ levels,
+                                                         const NodeCfg* __restrict__ cfg,
+                                                         const double4* __restrict__ pcost,
+                                                         const double* __restrict__ histp,
+                                                         const double* __restrict__ thr_tab,
+                                                         const int32_t* __restrict__ thr_row,
+                                                         DpScalars S, double2* __restrict__ phi) {
+  __shared__ double s_p[kPhiG][kPhiBins];  // nonzero bins in summation order
+  __shared__ int s_m[kPhiG][kPhiBins];     // ... their m = D - d
+  __shared__ int s_nnz[kPhiG];
+  const LevelDesc L = levels[lv_list[blockIdx.y]];
+  const int p0 = blockIdx.x * kPhiG;
+  if (p0 >= L.prev_count) return;
+  const int ng = min(kPhiG, L.prev_count - p0);
+  const int ncnt = L.next_count;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < ng) {  // warp g compacts prev p0 + g's nonzero bins, d descending
+    const NodeCfg pv = cfg[L.prev_base + p0 + warp];
+    const int dmax = pv.d > 0 ? min(L.k, pv.d) : -1;
+    int cnt = -1;  // -1: not staged (suspended prev, or a row past kPhiBins)
+    if (dmax >= 0 && dmax < kPhiBins) {
+      const double* hp = histp + pv.hist_off;
+      cnt = 0;
+      for (int c0 = dmax; c0 >= 0; c0 -= 32) {
+        const int d = c0 - lane;
+        const double v = d >= 0 ? hp[d] : 0.0;
+        const unsigned nz = __ballot_sync(0xffffffffu, v != 0.0);
+        if (v != 0.0) {
+          const int at = cnt + __popc(nz & ((1u << lane) - 1u));
+          s_p[warp][at] = v;
+          s_m[warp][at] = pv.d - d;
+        }
+        cnt += __popc(nz);
+      }
+    }
+    if (lane == 0) s_nnz[warp] = cnt;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncnt; i += blockDim.x) {
+    const NodeCfg nx = cfg[L.next_base + i];
+    NodeCost nc{0.0, 0.0, 0.0, 0.0};
+    if (nx.d > 0) {
+      const double4 c = pcost[nx.p];
+      nc.thr = thr_tab[thr_row[nx.p] + nx.d];
+      nc.pipe = c.x;
+      nc.unit = c.y;
+      nc.resume = c.z;
+    }
+    const PhiConst K = phi_const(L, S, nc);
+    const double rate = nc.thr;
+    for (int g = 0; g < ng; ++g) {
+      const NodeCfg pv = cfg[L.prev_base + p0 + g];
+      const int nnz = s_nnz[g];
+      PhiOut o{0.0, 0.0};
+      if (nx.d <= 0 || pv.d <= 0 || S.strict || nnz < 0) {
+        o = phi_dev(pv, nx, nc, L, S, ProbPtr{histp + pv.hist_off}, thr_tab, thr_row, K);
+      } else if (nx.p != pv.p) {  // depth change: c_pipe for m >= 1, rollback for m = 0
+        double committed = 0.0, cost_sum = 0.0;
+        for (int q = 0; q < nnz; ++q) {
+          const double pr = s_p[g][q];
+          const bool rb = s_m[g][q] == 0;
+          committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr, rate), rb ? K.teff_rb : K.teff_pipe));
+          cost_sum = __dadd_rn(cost_sum, __dmul_rn(pr, rb ? K.c_rb : K.c_pipe));
+        }
+        o = PhiOut{committed, cost_sum};
+      } else {  // same depth: phi_dev's branch-free per-bin transition cost
+        const int sd = pv.d, td = nx.d;
+        double committed = 0.0, cost_sum = 0.0;
+        for (int q = 0; q < nnz; ++q) {
+          const double pr = s_p[g][q];
+          const int m = s_m[g][q];
+          const int mm = m > 0 ? m : 1;
+          int r = 0;
+          if (td > mm) {
+            r = __clz(mm) - __clz(td);
+            r += ((mm << r) < td) ? 1 : 0;
+          }
+          const double inter_a = __dmul_rn(static_cast<double>(r), nc.unit);
+          const double inter = (nc.pipe < inter_a) ? nc.pipe : inter_a;
+          const double c_rep = __dadd_rn(K.base, inter);
+          double cost = (r == 0) ? ((m >= sd && td == sd) ? 0.0 : K.base) : c_rep;
+          cost = (m == 0) ? K.c_rb : cost;
+          const double te = __dsub_rn(S.T, cost);
+          double t_eff = (0.0 < te) ? te : 0.0;
+          t_eff = (m == 0) ? K.teff_rb : t_eff;
+          committed = __dadd_rn(committed, __dmul_rn(__dmul_rn(pr, rate), t_eff));
+          cost_sum = __dadd_rn(cost_sum, __dmul_rn(pr, cost));
+        }
+        o = PhiOut{committed, cost_sum};
+      }
+      phi[static_cast<int64_t>(L.phi_off) + static_cast<int64_t>(p0 + g) * ncnt + i] =
+          make_double2(o.committed, o.mig);
+    }
+  }
+}
+
+// The level step over materialised phi: F_{j+1}[c'] = max_c F_j[c] +
+// phi(c, c'), a max-plus pass with the reference's take order.  A warp per
+// next node (eight per block, so a level needs few SM slots while the
+// sampling still runs), lanes over the prevs (a column of the prev-major phi
+// block) with four loads in flight per lane, then a shuffle arg-max.  phi is
+// fetched before griddepcontrol.wait (it was complete before this level's
+// event wait), the previous level's values after it.
+__global__ void __launch_bounds__(256) dp_maxplus_kernel(int j, const LevelDesc* __restrict__ levels,
+                                                         const double2* __restrict__ phi,
+                                                         double* __restrict__ val, double* __restrict__ mig,
+                                                         int32_t* __restrict__ parent,
+                                                         double* __restrict__ stc, double* __restrict__ stm) {
+  constexpr int kU = 4;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const LevelDesc L = levels[j];
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const bool live = i < L.next_count;
+  const int pc = L.prev_count;
+  const int64_t ncnt = L.next_count;
+  const double2* col = phi + static_cast<int64_t>(L.phi_off) + i;
+  double2 f[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int pi = lane + 32 * u;
+    f[u] = live && pi < pc ? col[pi * ncnt] : make_double2(0.0, 0.0);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // level j-1's val / mig
+  if (!live) return;
+  const double* pval = val + L.prev_base;
+  const double* pmig = mig + L.prev_base;
+  Cand best{0.0, 0.0, 0.0, 0.0, -1};
+  auto take = [&](int pi, double v0, double m0, const double2& ph) {
+    const double v = __dadd_rn(v0, ph.x);
+    const double mg = __dadd_rn(m0, ph.y);
+    if (best.idx < 0 || v > best.value || (v == best.value && mg < best.mig)) {
+      best.value = v;
+      best.mig = mg;
+      best.stc = ph.x;
+      best.stm = ph.y;
+      best.idx = pi;
+    }
+  };
+  for (int p0 = 0; p0 < pc; p0 += 32 * kU) {
+    double v[kU], m[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pi = p0 + lane + 32 * u;
+      if (p0 > 0) f[u] = pi < pc ? col[pi * ncnt] : make_double2(0.0, 0.0);
+      v[u] = pi < pc ? pval[pi] : 0.0;
+      m[u] = pi < pc ? pmig[pi] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pi = p0 + lane + 32 * u;
+      if (pi < pc) take(pi, v[u], m[u], f[u]);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const Cand o = shfl_cand(best, lane ^ off);
+    if (cand_better(o, best)) best = o;
+  }
+  if (lane == 0) {
+    const int ni = L.next_base + i;
+    val[ni] = best.value;
+    mig[ni] = best.mig;
+    parent[ni] = best.idx;
+    stc[ni] = best.stc;
+    stm[ni] = best.stm;
+  }
+}
+
 // Final pick (rank = (value, -mig, D, -P), suspended = (-1, 0), first index
-// wins) and traceback into PlanStep[horizon].  One block of 256 threads.
-__global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restrict__ levels,
-                                                       int horizon,
-                                                       const NodeCfg* __restrict__ cfg,
-                                                       const double* __restrict__ val,
-                                                       const double* __restrict__ mig,
-                                                       const int32_t* __restrict__ parent,
-                                                       const double* __restrict__ stc,
-                                                       const double* __restrict__ stm,
-                                                       lp_plan_step* __restrict__ plan,
-                                                       double* __restrict__ final_value) {
-  __shared__ int s_idx[256];
+// wins) and traceback into PlanStep[horizon], by one block of 256 threads.
+// With s_dyn (n_nodes +
+// 2 * horizon ints of shared memory) every back-pointer is staged first, so
+// the serial walk costs a shared-memory load per level instead of an L2
+// round trip, and the plan rows are then written in parallel.
+__device__ void final_pick_traceback(const LevelDesc* __restrict__ levels, int horizon,
+                                     const NodeCfg* __restrict__ cfg, const double* val, const double* mig,
+                                     const int32_t* parent, const double* stc, const double* stm,
+                                     lp_plan_step* __restrict__ plan, double* __restrict__ final_value,
+                                     int* s_idx, int* s_dyn, int n_nodes) {
   const LevelDesc last = levels[horizon - 1];
   const int base = last.next_base, cnt = last.next_count;
   auto gt = [&](int a, int b) -> bool {  // rank(a) > rank(b)
     if (b < 0) return a >= 0;
     if (a < 0) return false;
-    const double va = val[base + a], vb = val[base + b];
+    const double va = __ldcg(val + base + a), vb = __ldcg(val + base + b);
     if (vb < va) return true;
     if (va < vb) return false;
-    const double ma = -mig[base + a], mb = -mig[base + b];
+    const double ma = -__ldcg(mig + base + a), mb = -__ldcg(mig + base + b);
     if (mb < ma) return true;
     if (ma < mb) return false;
     const NodeCfg ca = cfg[base + a], cb = cfg[base + b];
@@ -453,6 +636,10 @@ __global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restri
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
     if (gt(i, mine)) mine = i;  // ascending i: strict > keeps the first
   s_idx[threadIdx.x] = mine;
+  if (s_dyn) {
+    for (int i = threadIdx.x; i < n_nodes; i += blockDim.x) s_dyn[i] = __ldcg(parent + i);
+    for (int jj = threadIdx.x; jj < horizon; jj += blockDim.x) s_dyn[n_nodes + jj] = levels[jj].next_base;
+  }
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
@@ -462,24 +649,77 @@ __global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restri
     }
     __syncthreads();
   }
+  auto row = [&](int jj, int gi) {  // plan step of interval jj (1-based)
+    const NodeCfg c = cfg[gi];
+    lp_plan_step st;
+    st.interval_index = jj;
+    st.config.pipelines = c.d > 0 ? c.d : 0;
+    st.config.stages = c.d > 0 ? c.p : 0;
+    st.expected_committed = __ldcg(stc + gi);
+    st.expected_mig_cost_s = __ldcg(stm + gi);
+    plan[jj - 1] = st;
+  };
+  if (s_dyn) {
+    const int* s_nb = s_dyn + n_nodes;
+    int* s_gi = s_dyn + n_nodes + horizon;
+    if (threadIdx.x == 0) {
+      int idx = s_idx[0];
+      if (final_value) *final_value = __ldcg(val + base + idx);
+      for (int jj = horizon; jj >= 1; --jj) {
+        const int gi = s_nb[jj - 1] + idx;
+        s_gi[jj - 1] = gi;
+        idx = s_dyn[gi];
+      }
+    }
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < horizon; jj += blockDim.x) row(jj + 1, s_gi[jj]);
+    return;
+  }
   if (threadIdx.x == 0) {
     int idx = s_idx[0];
-    if (final_value) *final_value = val[base + idx];
+    if (final_value) *final_value = __ldcg(val + base + idx);
     for (int jj = horizon; jj >= 1; --jj) {
-      const LevelDesc Lj = levels[jj - 1];
-      const int gi = Lj.next_base + idx;
-      const NodeCfg c = cfg[gi];
-      lp_plan_step st;
-      st.interval_index = jj;
-      st.config.pipelines = c.d > 0 ? c.d : 0;
-      st.config.stages = c.d > 0 ? c.p : 0;
-      st.expected_committed = stc[gi];
-      st.expected_mig_cost_s = stm[gi];
-      plan[jj - 1] = st;
-      idx = parent[gi];
+      const int gi = levels[jj - 1].next_base + idx;
+      row(jj, gi);
+      idx = __ldcg(parent + gi);
     }
   }
 }
+
+__global__ void __launch_bounds__(256) dp_final_kernel(const LevelDesc* __restrict__ levels, int horizon,
+                                                       const NodeCfg* __restrict__ cfg, const double* val,
+                                                       const double* mig, const int32_t* parent,
+                                                       const double* stc, const double* stm,
+                                                       lp_plan_step* __restrict__ plan,
+                                                       double* __restrict__ final_value, int n_nodes) {
+  __shared__ int s_idx[256];
+  extern __shared__ int s_dyn[];
+  final_pick_traceback(levels, horizon, cfg, val, mig, parent, stc, stm, plan, final_value, s_idx,
+                       n_nodes > 0 ? s_dyn : nullptr, n_nodes);
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Monotone arrival counter (zeroed before the launch): a barrier completes
+// when the counter reaches `target`, the running total of the blocks taking
+// part in every barrier so far (all blocks for the first, the level blocks
+// after it).
+__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    while (ld_relaxed_u32(ctr) < target) __nanosleep(32);
+    __threadfence();  // acquire: orders the block's later reads after the arrivals
+  }
+  __syncthreads();
+}
+
+
 
 // Liveput table: for each (level with histogram, prev config) row,
 // sum_m count_m * throughput(m, P) / count (expected_liveput semantics,
@@ -563,6 +803,32 @@ cudaError_t launch_dp_step(int j, int next_count, int prev_count, bool pdl, cuda
                             parent, stc, stm);
 }
 
+cudaError_t launch_phi_matrix(int n_levels, int64_t max_pairs, cudaStream_t st, const int32_t* lv_list,
+                              const LevelDesc* levels, const NodeCfg* cfg, const double4* pcost,
+                              const double* histp, const double* thr_tab, const int32_t* thr_row,
+                              const DpScalars& S, double2* phi) {
+  if (n_levels <= 0 || max_pairs <= 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((max_pairs + kPhiG - 1) / kPhiG), static_cast<unsigned>(n_levels));  // max_pairs: largest prev count
+  phi_matrix_kernel<<<grid, 256, 0, st>>>(lv_list, levels, cfg, pcost, histp, thr_tab, thr_row, S, phi);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dp_maxplus(int j, int next_count, bool pdl, cudaStream_t st, const LevelDesc* levels,
+                              const double2* phi, double* val, double* mig, int32_t* parent, double* stc,
+                              double* stm) {
+  if (next_count <= 0) return cudaSuccess;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((next_count + 7) / 8);
+  lc.blockDim = dim3(256);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, dp_maxplus_kernel, j, levels, phi, val, mig, parent, stc, stm);
+}
+
 cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
                              const EntryDesc* ents, const uint32_t* hist, const int32_t* store_off,
                              double* store) {
@@ -571,12 +837,23 @@ cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pai
   return cudaGetLastError();
 }
 
+// dynamic shared memory of the staged traceback (0: the walk reads L2)
+static size_t trace_smem(int n_nodes, int horizon) {
+  const size_t b = static_cast<size_t>(n_nodes + 2 * horizon) * sizeof(int);
+  return b <= 160 * 1024 ? b : 0;
+}
+
 cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
                             const NodeCfg* cfg, const double* val, const double* mig,
                             const int32_t* parent, const double* stc, const double* stm,
-                            lp_plan_step* plan, double* final_value) {
-  dp_final_kernel<<<1, 256, 0, st>>>(levels, horizon, cfg, val, mig, parent, stc, stm, plan,
-                                     final_value);
+                            lp_plan_step* plan, double* final_value, int n_nodes) {
+  const size_t smem = n_nodes > 0 ? trace_smem(n_nodes, horizon) : 0;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = smem_optin(reinterpret_cast<const void*>(dp_final_kernel), smem);
+    if (e != cudaSuccess) return e;
+  }
+  dp_final_kernel<<<1, 256, smem, st>>>(levels, horizon, cfg, val, mig, parent, stc, stm, plan,
+                                        final_value, smem ? n_nodes : 0);
   return cudaGetLastError();
 }
 
@@ -604,28 +881,6 @@ cudaError_t launch_phi_single(const NodeCfg& pv, const NodeCfg& nx, const NodeCo
 // H + 2 kernel boundaries.  Values written inside the launch (probabilities,
 // val/mig/parent/step terms) are read back through L2 (ld.cg) or after a
 // barrier that follows their only writes, never through the read-only path.
-
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Monotone arrival counter (zeroed before the launch): a barrier completes
-// when the counter reaches `target`, the running total of the blocks taking
-// part in every barrier so far (all blocks for the first, the level blocks
-// after it).
-__device__ __forceinline__ void grid_barrier(uint32_t* ctr, uint32_t target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    while (ld_relaxed_u32(ctr) < target) __nanosleep(32);
-    __threadfence();  // acquire: orders the block's later reads after the arrivals
-  }
-  __syncthreads();
-}
-
 
 // STAGED (small re-plans, N ~ 16..48): every block copies the node list, its
 // own next nodes' cost terms for every level, and all prev probability rows

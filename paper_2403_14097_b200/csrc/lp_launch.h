@@ -58,13 +58,23 @@ cudaError_t launch_dp_step(int j, int next_count, int prev_count, bool pdl, cuda
                            const NodeCfg* cfg, const double4* pcost, const double* histp,
                            const double* thr_tab, const int32_t* thr_row, const DpScalars& S,
                            double* val, double* mig, int32_t* parent, double* stc, double* stm);
+// Materialised phi (pipelined re-plans): every (next, prev) pair of the
+// levels in lv_list[0..n_levels), then the per-level max-plus pass over it.
+cudaError_t launch_phi_matrix(int n_levels, int64_t max_pairs, cudaStream_t st, const int32_t* lv_list,
+                              const LevelDesc* levels, const NodeCfg* cfg, const double4* pcost,
+                              const double* histp, const double* thr_tab, const int32_t* thr_row,
+                              const DpScalars& S, double2* phi);
+cudaError_t launch_dp_maxplus(int j, int next_count, bool pdl, cudaStream_t st, const LevelDesc* levels,
+                              const double2* phi, double* val, double* mig, int32_t* parent, double* stc,
+                              double* stm);
 cudaError_t launch_normalize(int n_entries, cudaStream_t st, const PairDesc* pairs,
                              const EntryDesc* ents, const uint32_t* hist, const int32_t* store_off,
                              double* store);
+// n_nodes > 0: stage every back-pointer in shared memory for the walk
 cudaError_t launch_dp_final(int horizon, cudaStream_t st, const LevelDesc* levels,
                             const NodeCfg* cfg, const double* val, const double* mig,
                             const int32_t* parent, const double* stc, const double* stm,
-                            lp_plan_step* plan, double* final_value);
+                            lp_plan_step* plan, double* final_value, int n_nodes = 0);
 cudaError_t launch_liveput(int n_rows, cudaStream_t st, const int4* rows, const LevelDesc* levels,
                            const NodeCfg* cfg, const uint32_t* hist, const double* probs,
                            const double* thr_tab, const int32_t* thr_row, lp_liveput_row* out);

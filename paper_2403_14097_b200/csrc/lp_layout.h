@@ -100,7 +100,7 @@ struct LevelDesc {
   int32_t next_base, next_count;   // node range of level j+1
   int32_t fresh;                   // n_next > n_now
   int32_t has_hist;
-  int32_t pad;
+  int32_t phi_off;                 // materialised phi: first (next, prev) pair, in double2
   uint64_t total;                  // ensemble size of the level's pair
   double fixed;                    // fresh > 0 ? fresh_fixed : 0.0
 };

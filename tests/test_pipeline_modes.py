@@ -2,7 +2,8 @@
 the persistent DP kernel, three pipelined stages with per-level DP launches,
 one stage per ensemble, the per-level launches alone (with and without
 programmatic dependent launch), and the persistent DP with and without its
-shared-memory staging of small re-plans, other DP block and work-item sizes, other row-kernel block shapes
+shared-memory staging of small re-plans, phi materialised ahead of max-plus
+levels or evaluated inside them, other DP block and work-item sizes, other row-kernel block shapes
 (small event tables split a pair's depths over many work items),
 and the alternative histogram kernels all give the same plan (configs and FP64 step values, bit for bit).  The mode switches are read
 once per process, so each mode runs in a subprocess."""
@@ -58,5 +59,11 @@ def test_execution_modes_agree():
                 {"LIVEPUT_DP_THREADS": "64"}, {"LIVEPUT_PER_BLOCK": "512"},
                 {"LIVEPUT_HIST_KERNEL": "legacy"}, {"LIVEPUT_HIST_KERNEL": "noinc"}, {"LIVEPUT_HIST_KERNEL": "inc"}, {"LIVEPUT_BITS_MAXK": "8"},
                 {"LIVEPUT_HIST_KERNEL": "norows"}, {"LIVEPUT_ROWS_SHAPE": "160,56,8"},
-                {"LIVEPUT_ROWS_SHAPE": "96,40,2"}, {"LIVEPUT_ROWS_KREG": "0"}):
+                {"LIVEPUT_ROWS_SHAPE": "96,40,2"}, {"LIVEPUT_ROWS_KREG": "0"},
+                # the materialised-phi DP (phi launches + max-plus levels) on every
+                # pipelined re-plan, per-level phi launches, one stage with level
+                # launches, and the per-rank-share threshold
+                {"LIVEPUT_PHI": "1"}, {"LIVEPUT_PHI": "1", "LIVEPUT_PHI_LEVELS": "1"},
+                {"LIVEPUT_PHI": "1", "LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"},
+                {"LIVEPUT_PHI": "1", "LIVEPUT_PDL": "0"}, {"LIVEPUT_PHI": "400000"}):
         assert _run(env) == base, env

@@ -63,3 +63,38 @@ def test_config3_proactive_replans_with_cache():
         p.set_hist_cache(True)
         for i, r in enumerate(c["replans"]):
             assert _rows(p.dp_optimize(_cfg(r["current"]), r["n_seq"])) == r["plan"], i
+
+
+@pytest.mark.gpu
+def test_materialised_phi_matches_fixtures():
+    """The multi-GPU DP path (phi launches per pipeline stage + max-plus
+    levels, an A/B path selected with LIVEPUT_PHI) on the
+    full 1e6 ensembles: forced with LIVEPUT_PHI=1, read once per
+    process, so it runs in a subprocess."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    names = ["bench", "ns12", "predict"]
+    script = (
+        "import json, sys\n"
+        f"sys.path.insert(0, {str(root)!r}); sys.path.insert(0, {str(root / 'tests')!r})\n"
+        "from conftest import load_golden\n"
+        "from paper_2403_14097_b200.model import CostTable, ParallelConfig, PlannerOptions, PROFILES\n"
+        "from paper_2403_14097_b200.planner import Planner\n"
+        "F = load_golden('plans_1e6'); out = {}\n"
+        f"for name in {names!r}:\n"
+        "    c = F[name]; cur = None if c['current'] is None else ParallelConfig(*c['current'])\n"
+        "    with Planner(PROFILES[c['profile']](), CostTable(), PlannerOptions(mc_trials=c['trials'])) as p:\n"
+        "        out[name] = [[None if s.config is None else [s.config.pipelines, s.config.stages],\n"
+        "                      s.expected_committed.hex(), s.expected_mig_cost_s.hex()]\n"
+        "                     for s in p.dp_optimize(cur, c['n_seq'])]\n"
+        "print(json.dumps(out))\n")
+    env = dict(os.environ, LIVEPUT_PHI="1")
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in names:
+        assert got[name] == FIX[name]["plan"], name
