@@ -228,7 +228,8 @@ struct HistPlan {
   std::vector<EntryDesc> entries;
   std::vector<DrawConst> draws;
   std::vector<uint64_t> binom;
-  std::vector<WorkItem> work;
+  std::vector<WorkSpan> spans;  // per-block WorkItems are expanded on the device
+  int64_t n_work = 0;           // blocks over all groups
   std::vector<uint16_t> divtab;
   std::vector<uint32_t> dmask;  // bits kernel: per (range, pass, d) depth-divisor masks
   size_t big_words = 0;         // n > kBigN: scratch words per thread of the big kernel
@@ -492,7 +493,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
 
   // work items, grouped by launch configuration
   // one record per (pair, entry range): its work items are the chunks of
-  // the pair's trial range, expanded straight into hp.work below
+  // the pair's trial range, one WorkSpan per range (blocks expanded on the device)
   struct Range {
     WorkItem w;  // t0 / t1 set per chunk
     uint64_t t_lo, t_hi, chunk;
@@ -786,12 +787,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     }
   }
   mark("items");
-  {
-    size_t total = 0;
-    for (const auto& [key, items] : groups)
-      for (const Range& r : items) total += (r.t_hi - r.t_lo + r.chunk - 1) / r.chunk;
-    hp.work.reserve(total);
-  }
+  int64_t nblk = 0;
   for (auto& [key, items] : groups) {
     Group g;
     g.stage = std::get<0>(key);
@@ -799,7 +795,7 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
     g.kmax = std::get<2>(key);
     g.threads = std::get<3>(key);
     g.smem_evt = std::get<4>(key) != 0;
-    g.first = (int)hp.work.size();
+    g.first = (int)nblk;
     for (const Range& r : items) g.pmax_cap = std::max(g.pmax_cap, r.aux);
     for (const Range& r : items) {
       size_t sm = r.smem;
@@ -809,16 +805,21 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
       if (g.kind == 1)
         sm = smem_ctr(r.w.e_hi - r.w.e_lo, pd.k, pd.n, r.w.evt_len, g.smem_evt, g.threads, g.pmax_cap);
       g.smem = std::max(g.smem, sm);
-      for (uint64_t t0 = r.t_lo; t0 < r.t_hi; t0 += r.chunk) {
-        WorkItem w = r.w;
-        w.t0 = t0;
-        w.t1 = std::min(r.t_hi, t0 + r.chunk);
-        hp.work.push_back(w);
-      }
+      if (r.t_hi <= r.t_lo) continue;
+      WorkSpan sp{};
+      sp.w = r.w;
+      sp.w.t0 = r.t_lo;
+      sp.w.t1 = r.t_hi;
+      sp.chunk = r.chunk;
+      sp.first = (int32_t)nblk;
+      hp.spans.push_back(sp);
+      nblk += (int64_t)((r.t_hi - r.t_lo + r.chunk - 1) / r.chunk);
     }
-    g.count = (int)hp.work.size() - g.first;
+    g.count = (int)(nblk - g.first);
     hp.groups.push_back(g);
   }
+  hp.n_work = nblk;
+  if (nblk > INT32_MAX) return LP_EUNSUPPORTED;
   mark("groups");
   // stage ranges (specs come with non-decreasing stages)
   int nst = 0;
@@ -847,14 +848,17 @@ struct HistDev {
   const EntryDesc* entries;
   const DrawConst* draws;
   const uint64_t* binom;
-  const WorkItem* work;
+  const WorkSpan* spans;
+  WorkItem* work;  // expanded from spans by the first launch of an execute
   uint32_t* evt;
   uint32_t* h0;
   uint32_t* hist;
 };
 
 cudaError_t run_hist(const HistPlan& hp, const HistDev& d, cudaStream_t st, int* launches) {
-  cudaError_t e;
+  cudaError_t e = launch_expand_work(d.spans, (int)hp.spans.size(), (int)hp.n_work, d.work, st);
+  if (e != cudaSuccess) return e;
+  if (hp.n_work > 0) ++*launches;
   if (hp.evt_len > 0) {
     e = cudaMemsetAsync(d.evt, 0, sizeof(uint32_t) * hp.evt_len, st);
     if (e != cudaSuccess) return e;
@@ -1036,6 +1040,7 @@ struct lp_handle {
          off_levels = 0, off_cfg = 0, off_cost = 0, off_lrows = 0, off_thr = 0, off_throw = 0,
          off_gather = 0, off_pbase = 0;
   std::vector<int32_t> dp_gather, dp_pbase;  // cluster DP staging lists
+  size_t w_items = 0;  // the expanded WorkItems of the histogram launches
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
          w_plan = 0, w_live = 0, w_final = 0, w_bar = 0;
   int max_next = 0;         // largest level (next role), for the persistent DP grid
@@ -1126,21 +1131,23 @@ lp_status upload_hist(lp_handle* h, const HistPlan& hp, DevBuf& tables, DevBuf& 
                       Packer& pk, std::vector<size_t>& extra_offs) {
   (void)extra_offs;
   const size_t op = pk.add(hp.pairs), oe = pk.add(hp.entries), od = pk.add(hp.draws),
-               ob = pk.add(hp.binom), ow = pk.add(hp.work), odt = pk.add(hp.divtab),
+               ob = pk.add(hp.binom), ow = pk.add(hp.spans), odt = pk.add(hp.divtab),
                odm = pk.add(hp.dmask);
   LP_CUDA(h, tables.ensure(pk.bytes.size()));
   LP_CUDA(h, h->pin_up.ensure(pk.bytes.size()));
   std::memcpy(h->pin_up.p, pk.bytes.data(), pk.bytes.size());
   LP_CUDA(h, cudaMemcpyAsync(tables.p, h->pin_up.p, pk.bytes.size(), cudaMemcpyHostToDevice,
                              h->stream));
-  const size_t wb = a16(4 * std::max<int64_t>(hp.evt_len, 1)) + a16(4 * std::max<int64_t>(hp.h0_len, 1)) +
-                    a16(4 * std::max<int64_t>(hp.hist_len, 1));
+  const size_t wb0 = a16(4 * std::max<int64_t>(hp.evt_len, 1)) + a16(4 * std::max<int64_t>(hp.h0_len, 1)) +
+                     a16(4 * std::max<int64_t>(hp.hist_len, 1));
+  const size_t wb = wb0 + a16(sizeof(WorkItem) * std::max<int64_t>(hp.n_work, 1));
   LP_CUDA(h, work.ensure(wb));
   d.pairs = dptr<PairDesc>(tables, op);
   d.entries = dptr<EntryDesc>(tables, oe);
   d.draws = dptr<DrawConst>(tables, od);
   d.binom = dptr<uint64_t>(tables, ob);
-  d.work = dptr<WorkItem>(tables, ow);
+  d.spans = dptr<WorkSpan>(tables, ow);
+  d.work = dptr<WorkItem>(work, wb0);
   d.divtab = dptr<uint16_t>(tables, odt);
   d.dmask = dptr<uint32_t>(tables, odm);
   {
@@ -1745,7 +1752,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     lp_status us = upload_image(h,
                                 {sec(h->hp.pairs, &h->off_pairs), sec(h->hp.entries, &h->off_entries),
                                  sec(h->hp.draws, &h->off_draws), sec(h->hp.binom, &h->off_binom),
-                                 sec(h->hp.work, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
+                                 sec(h->hp.spans, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
                                  sec(h->hp.dmask, &h->off_dmask),
                                  sec(h->store_off, &h->off_store_off)},
                                 h->tables, h->pin_up, h->ev_up[0], &bytes, h->stream);
@@ -1763,6 +1770,7 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
   h->w_evt = take(4 * std::max<int64_t>(h->hp.evt_len, 1));
   h->w_h0 = take(4 * std::max<int64_t>(h->hp.h0_len, 1));
   h->w_hist = take(4 * std::max<int64_t>(h->hp.hist_len, 1));
+  h->w_items = take(sizeof(WorkItem) * std::max<int64_t>(h->hp.n_work, 1));
   h->w_val = take(8 * nn);
   h->w_mig = take(8 * nn);
   h->w_par = take(4 * nn);
@@ -2007,7 +2015,8 @@ lp_status exec_hist(lp_handle* h) {
   d.entries = dptr<EntryDesc>(h->tables, h->off_entries);
   d.draws = dptr<DrawConst>(h->tables, h->off_draws);
   d.binom = dptr<uint64_t>(h->tables, h->off_binom);
-  d.work = dptr<WorkItem>(h->tables, h->off_work);
+  d.spans = dptr<WorkSpan>(h->tables, h->off_work);
+  d.work = dptr<WorkItem>(h->work, h->w_items);
   d.divtab = dptr<uint16_t>(h->tables, h->off_divtab);
   d.dmask = dptr<uint32_t>(h->tables, h->off_dmask);
   {
@@ -2024,6 +2033,8 @@ lp_status exec_hist(lp_handle* h) {
   const bool norm_here = nst > 1 || h->dp_launches || h->horizon > kMaxHorizon;
   int launches = 0;
   LP_CUDA(h, cudaEventRecord(h->ev[0], st));
+  LP_CUDA(h, launch_expand_work(d.spans, (int)hp.spans.size(), (int)hp.n_work, d.work, st));
+  if (hp.n_work > 0) ++launches;
   if (hp.evt_len > 0) LP_CUDA(h, cudaMemsetAsync(d.evt, 0, sizeof(uint32_t) * hp.evt_len, st));
   LP_CUDA(h, cudaMemsetAsync(d.h0, 0, sizeof(uint32_t) * std::max<int64_t>(hp.h0_len, 1), st));
   // The stages' histogram kernels go out at once, each on its own stream,

@@ -392,6 +392,31 @@ cudaError_t launch_hist_ctr(bool smem_evt, int blocks, int threads, size_t smem,
 }
 
 // Finalize of a stage: pairs [p0, p0 + n_pairs), entries [e0, e0 + n_entries).
+// One thread per block of the histogram launches: its WorkItem from the
+// span holding it (binary search over the spans' first blocks).
+__global__ void expand_work_kernel(const WorkSpan* __restrict__ spans, int n_spans, int n_work,
+                                   WorkItem* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_work) return;
+  int lo = 0, hi = n_spans - 1;  // last span with first <= b
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (spans[mid].first <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const WorkSpan sp = spans[lo];
+  WorkItem w = sp.w;
+  w.t0 = sp.w.t0 + static_cast<uint64_t>(b - sp.first) * sp.chunk;
+  w.t1 = min(sp.w.t1, w.t0 + sp.chunk);
+  out[b] = w;
+}
+
+cudaError_t launch_expand_work(const WorkSpan* spans, int n_spans, int n_work, WorkItem* out, cudaStream_t st) {
+  if (n_work <= 0) return cudaSuccess;
+  expand_work_kernel<<<(n_work + 255) / 256, 256, 0, st>>>(spans, n_spans, n_work, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize_range(int p0, int n_pairs, int e0, int n_entries, cudaStream_t st,
                                   const PairDesc* pairs, const EntryDesc* ents, uint32_t* evt,
                                   uint32_t* h0, uint32_t* hist) {

@@ -42,6 +42,8 @@ cudaError_t launch_hist_rows(int kreg, int wmax, bool smem_evt, int blocks, int 
                              size_t smem, cudaStream_t st, const WorkItem* w,
                              const PairDesc* pairs, const EntryDesc* ents, const DrawConst* dr,
                              const uint64_t* binom, uint32_t* evt, uint32_t* h0);
+// per-block WorkItems of the histogram launches from the uploaded spans
+cudaError_t launch_expand_work(const WorkSpan* spans, int n_spans, int n_work, WorkItem* out, cudaStream_t st);
 cudaError_t launch_finalize_range(int p0, int n_pairs, int e0, int n_entries, cudaStream_t st,
                                   const PairDesc* pairs, const EntryDesc* ents, uint32_t* evt,
                                   uint32_t* h0, uint32_t* hist);

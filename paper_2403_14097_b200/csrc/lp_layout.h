@@ -72,6 +72,17 @@ struct WorkItem {
   uint64_t t0, t1;      // scenario range
 };
 
+// A run of consecutive blocks over one scenario range: block first + b
+// takes scenarios [w.t0 + b * chunk, min(w.t1, w.t0 + (b + 1) * chunk)).
+// The host uploads the spans (a few per ensemble) and one kernel expands
+// them into per-block WorkItems on the device.
+struct WorkSpan {
+  WorkItem w;           // t0 / t1: the whole range
+  uint64_t chunk;
+  int32_t first;        // first block
+  int32_t pad;
+};
+
 // Row offset of D inside an entry's histogram block: rows hold
 // d = 0..min(k, D) (m = D - d).
 __host__ __device__ inline int32_t hist_row(int32_t D, int32_t k) {
