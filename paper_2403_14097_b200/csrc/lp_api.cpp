@@ -230,6 +230,7 @@ struct HistPlan {
   std::vector<uint64_t> binom;
   std::vector<WorkSpan> spans;  // per-block WorkItems are expanded on the device
   int64_t n_work = 0;           // blocks over all groups
+  std::vector<WorkItem> items;  // small plans (<= kHostItems blocks): expanded here, no expand launch
   std::vector<uint16_t> divtab;
   std::vector<uint32_t> dmask;  // bits kernel: per (range, pass, d) depth-divisor masks
   size_t big_words = 0;         // n > kBigN: scratch words per thread of the big kernel
@@ -247,6 +248,8 @@ struct HistPlan {
   uint64_t model_ops = 0;  // int ops of the algorithms actually run (op_model_*)
   int mc_pairs = 0, exact_pairs = 0;
 };
+
+constexpr int64_t kHostItems = 256;
 
 int kmax_for(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : 16); }
 
@@ -820,6 +823,14 @@ lp_status build_hist_plan(const std::vector<EnsembleSpec>& specs, int rank, int 
   }
   hp.n_work = nblk;
   if (nblk > INT32_MAX) return LP_EUNSUPPORTED;
+  if (nblk <= kHostItems)  // latency-bound small re-plans: one launch fewer
+    for (const WorkSpan& sp : hp.spans)
+      for (uint64_t t0 = sp.w.t0; t0 < sp.w.t1; t0 += sp.chunk) {
+        WorkItem w = sp.w;
+        w.t0 = t0;
+        w.t1 = std::min(sp.w.t1, t0 + sp.chunk);
+        hp.items.push_back(w);
+      }
   mark("groups");
   // stage ranges (specs come with non-decreasing stages)
   int nst = 0;
@@ -1041,6 +1052,7 @@ struct lp_handle {
          off_gather = 0, off_pbase = 0;
   std::vector<int32_t> dp_gather, dp_pbase;  // cluster DP staging lists
   size_t w_items = 0;  // the expanded WorkItems of the histogram launches
+  size_t off_items = 0;  // ... or the host-expanded ones of a small plan
   size_t w_evt = 0, w_h0 = 0, w_hist = 0, w_val = 0, w_mig = 0, w_par = 0, w_stc = 0, w_stm = 0,
          w_plan = 0, w_live = 0, w_final = 0, w_bar = 0;
   int max_next = 0;         // largest level (next role), for the persistent DP grid
@@ -1752,7 +1764,8 @@ lp_status prepare_hist(lp_handle* h, lp_config current, const int32_t* n_seq, in
     lp_status us = upload_image(h,
                                 {sec(h->hp.pairs, &h->off_pairs), sec(h->hp.entries, &h->off_entries),
                                  sec(h->hp.draws, &h->off_draws), sec(h->hp.binom, &h->off_binom),
-                                 sec(h->hp.spans, &h->off_work), sec(h->hp.divtab, &h->off_divtab),
+                                 sec(h->hp.spans, &h->off_work), sec(h->hp.items, &h->off_items),
+                                 sec(h->hp.divtab, &h->off_divtab),
                                  sec(h->hp.dmask, &h->off_dmask),
                                  sec(h->store_off, &h->off_store_off)},
                                 h->tables, h->pin_up, h->ev_up[0], &bytes, h->stream);
@@ -2008,6 +2021,8 @@ lp_status prepare_dp(lp_handle* h) {
 
 // execute, part 1: histogram kernels, the cross-rank sum, normalisation
 // into the probability store.  Needs only prepare_hist's image.
+bool hp_small(const lp_handle* h) { return !h->hp.items.empty(); }
+
 lp_status exec_hist(lp_handle* h) {
   cudaStream_t st = h->stream;
   HistDev d{};
@@ -2016,7 +2031,7 @@ lp_status exec_hist(lp_handle* h) {
   d.draws = dptr<DrawConst>(h->tables, h->off_draws);
   d.binom = dptr<uint64_t>(h->tables, h->off_binom);
   d.spans = dptr<WorkSpan>(h->tables, h->off_work);
-  d.work = dptr<WorkItem>(h->work, h->w_items);
+  d.work = hp_small(h) ? dptr<WorkItem>(h->tables, h->off_items) : dptr<WorkItem>(h->work, h->w_items);
   d.divtab = dptr<uint16_t>(h->tables, h->off_divtab);
   d.dmask = dptr<uint32_t>(h->tables, h->off_dmask);
   {
@@ -2033,8 +2048,10 @@ lp_status exec_hist(lp_handle* h) {
   const bool norm_here = nst > 1 || h->dp_launches || h->horizon > kMaxHorizon;
   int launches = 0;
   LP_CUDA(h, cudaEventRecord(h->ev[0], st));
-  LP_CUDA(h, launch_expand_work(d.spans, (int)hp.spans.size(), (int)hp.n_work, d.work, st));
-  if (hp.n_work > 0) ++launches;
+  if (!hp_small(h)) {
+    LP_CUDA(h, launch_expand_work(d.spans, (int)hp.spans.size(), (int)hp.n_work, d.work, st));
+    if (hp.n_work > 0) ++launches;
+  }
   if (hp.evt_len > 0) LP_CUDA(h, cudaMemsetAsync(d.evt, 0, sizeof(uint32_t) * hp.evt_len, st));
   LP_CUDA(h, cudaMemsetAsync(d.h0, 0, sizeof(uint32_t) * std::max<int64_t>(hp.h0_len, 1), st));
   // The stages' histogram kernels go out at once, each on its own stream,
