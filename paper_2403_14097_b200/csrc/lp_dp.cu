@@ -616,39 +616,52 @@ __device__ void final_pick_traceback(const LevelDesc* __restrict__ levels, int h
                                      int* s_idx, int* s_dyn, int n_nodes) {
   const LevelDesc last = levels[horizon - 1];
   const int base = last.next_base, cnt = last.next_count;
-  auto gt = [&](int a, int b) -> bool {  // rank(a) > rank(b)
-    if (b < 0) return a >= 0;
-    if (a < 0) return false;
-    const double va = __ldcg(val + base + a), vb = __ldcg(val + base + b);
-    if (vb < va) return true;
-    if (va < vb) return false;
-    const double ma = -__ldcg(mig + base + a), mb = -__ldcg(mig + base + b);
-    if (mb < ma) return true;
-    if (ma < mb) return false;
-    const NodeCfg ca = cfg[base + a], cb = cfg[base + b];
-    const int da = ca.d > 0 ? ca.d : -1, db = cb.d > 0 ? cb.d : -1;
-    if (db < da) return true;
-    if (da < db) return false;
-    const int pa = ca.d > 0 ? -ca.p : 0, pb = cb.d > 0 ? -cb.p : 0;
-    return pb < pa;
+  // rank = (value, -mig, D, -P), suspended (-1, 0); the first index wins
+  // ties.  Each thread scans its nodes in ascending order (strict > keeps
+  // the first), then the keys are reduced in registers: warp shuffles, then
+  // one slot per warp in shared memory.
+  struct Key {
+    double v, nm;
+    int d, np, idx;
   };
-  int mine = -1;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-    if (gt(i, mine)) mine = i;  // ascending i: strict > keeps the first
-  s_idx[threadIdx.x] = mine;
+  auto better = [](const Key& a, const Key& b) -> bool {  // a ranks above b (b.idx < 0: empty)
+    if (a.idx < 0) return false;
+    if (b.idx < 0) return true;
+    if (a.v != b.v) return b.v < a.v;
+    if (a.nm != b.nm) return b.nm < a.nm;
+    if (a.d != b.d) return b.d < a.d;
+    if (a.np != b.np) return b.np < a.np;
+    return a.idx < b.idx;
+  };
+  Key mine{0.0, 0.0, 0, 0, -1};
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const NodeCfg c = cfg[base + i];
+    const Key k{__ldcg(val + base + i), -__ldcg(mig + base + i), c.d > 0 ? c.d : -1, c.d > 0 ? -c.p : 0, i};
+    if (better(k, mine)) mine = k;
+  }
   if (s_dyn) {
     for (int i = threadIdx.x; i < n_nodes; i += blockDim.x) s_dyn[i] = __ldcg(parent + i);
     for (int jj = threadIdx.x; jj < horizon; jj += blockDim.x) s_dyn[n_nodes + jj] = levels[jj].next_base;
   }
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      const int a = s_idx[threadIdx.x], b = s_idx[threadIdx.x + s];
-      // ties between different threads' winners: lower index wins
-      if (gt(b, a) || (b >= 0 && a >= 0 && !gt(a, b) && b < a)) s_idx[threadIdx.x] = b;
-    }
-    __syncthreads();
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    Key o;
+    o.v = __shfl_xor_sync(0xffffffffu, mine.v, off);
+    o.nm = __shfl_xor_sync(0xffffffffu, mine.nm, off);
+    o.d = __shfl_xor_sync(0xffffffffu, mine.d, off);
+    o.np = __shfl_xor_sync(0xffffffffu, mine.np, off);
+    o.idx = __shfl_xor_sync(0xffffffffu, mine.idx, off);
+    if (better(o, mine)) mine = o;
   }
+  __shared__ Key s_key[32];
+  if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (better(s_key[w], mine)) mine = s_key[w];
+    s_idx[0] = mine.idx;
+  }
+  __syncthreads();
   auto row = [&](int jj, int gi) {  // plan step of interval jj (1-based)
     const NodeCfg c = cfg[gi];
     lp_plan_step st;
