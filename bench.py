@@ -261,7 +261,7 @@ def run_reference(args):
         value = tot_r / tot_s
         line = {"impl": "reference", "metric": "liveput scenarios/sec", "value": value, "unit": "resolutions/s",
                 "n_gpus": args.gpus, "steps": steps, "warmup": warm, "higher_is_better": True,
-                "ms_per_step": tot_s * 1000.0 / steps, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64",
+                "ms_per_step": tot_s * 1000.0 / steps, "scaling": "strong", "vs_baseline": None, "dtype": "int64/f64",
                 "data": "synthetic availability sequence (no dataset)",
                 "config": workload_config(args, n_seq),
                 "cpu_baseline": {"value": value, "unit": "resolutions/s", "cores": arm.threads, "kind": "reference",
@@ -440,7 +440,7 @@ def main():
     line = {
         "metric": "liveput scenarios/sec", "value": value, "unit": "resolutions/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 int + f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 int + f64",
         "data": "synthetic availability sequence and random-seeded MC scenarios (no dataset)",
         "config": workload_config(args, n_seq),
         "replan_ms": ms_per_step,
