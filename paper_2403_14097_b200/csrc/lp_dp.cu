@@ -1429,4 +1429,15 @@ cudaError_t launch_dp_cluster(cudaStream_t st, const DpArgs& a, const DpScalars&
   return cudaGetLastError();
 }
 
+void preload_dp() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, normalize_kernel);
+  cudaFuncGetAttributes(&a, dp_step_kernel);
+  cudaFuncGetAttributes(&a, dp_final_kernel);
+  cudaFuncGetAttributes(&a, liveput_kernel);
+  cudaFuncGetAttributes(&a, dp_persistent_kernel<true>);
+  cudaFuncGetAttributes(&a, dp_persistent_kernel<false>);
+  cudaFuncGetAttributes(&a, dp_cluster_kernel);
+}
+
 }  // namespace lp

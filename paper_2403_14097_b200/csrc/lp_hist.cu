@@ -452,4 +452,11 @@ cudaError_t launch_dump(int n, int k, int exact, int trials, uint64_t seed, cons
   return cudaGetLastError();
 }
 
+void preload_hist() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, h0_scan_kernel);
+  cudaFuncGetAttributes(&a, finalize_kernel);
+  cudaFuncGetAttributes(&a, expand_work_kernel);
+}
+
 }  // namespace lp

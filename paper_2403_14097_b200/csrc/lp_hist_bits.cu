@@ -265,4 +265,14 @@ cudaError_t launch_hist_bits(int kmax, bool smem_evt, int blocks, int threads, s
   return cudaErrorInvalidValue;
 }
 
+void preload_bits() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, hist_bits_kernel<16, 1, true>);
+  cudaFuncGetAttributes(&a, hist_bits_kernel<8, 1, true>);
+  cudaFuncGetAttributes(&a, hist_bits_kernel<4, 1, true>);
+  cudaFuncGetAttributes(&a, hist_bits_kernel<16, 1, false>);
+  cudaFuncGetAttributes(&a, hist_bits_kernel<8, 1, false>);
+  cudaFuncGetAttributes(&a, hist_bits_kernel<4, 1, false>);
+}
+
 }  // namespace lp

@@ -589,4 +589,14 @@ cudaError_t launch_hist_rows(int kreg, int wmax, bool smem_evt, int blocks, int 
   return cudaErrorInvalidValue;
 }
 
+// Load the row kernels' code now (lazy module loading would otherwise load
+// each on its first launch, inside the first re-plan that uses it).
+void preload_rows() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, hist_rows_kernel<0, 4, true>);
+  cudaFuncGetAttributes(&a, hist_rows_kernel<0, 4, false>);
+  cudaFuncGetAttributes(&a, hist_rows_kernel<16, 4, true>);
+  cudaFuncGetAttributes(&a, hist_rows_kernel<0, 8, true>);
+}
+
 }  // namespace lp

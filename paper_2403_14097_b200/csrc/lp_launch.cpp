@@ -34,4 +34,18 @@ cudaError_t smem_optin(const void* fn, size_t smem) {
   return e;
 }
 
+void preload_kernels() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  static std::mutex mu;
+  static std::unordered_map<int, bool> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return;
+  done[dev] = true;
+  preload_rows();
+  preload_bits();
+  preload_hist();
+  preload_dp();
+}
+
 }  // namespace lp

@@ -11,6 +11,15 @@ namespace lp {
 // Raise a kernel's dynamic shared-memory opt-in once per (device, kernel).
 cudaError_t smem_optin(const void* fn, size_t smem);
 
+// Load the default path's kernels on the current device (once per process
+// and device, from lp_create): lazy module loading would otherwise load each
+// inside the first re-plan that launches it.
+void preload_kernels();
+void preload_rows();
+void preload_bits();
+void preload_hist();
+void preload_dp();
+
 cudaError_t launch_hist_regs(int kmax, bool smem_evt, int blocks, size_t smem, cudaStream_t st,
                              const WorkItem* w, const PairDesc* pairs, const EntryDesc* ents,
                              const DrawConst* dr, const uint64_t* binom, uint32_t* evt,
