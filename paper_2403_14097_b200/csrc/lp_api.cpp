@@ -1395,16 +1395,17 @@ lp_status lp_create(const lp_profile* profile, const lp_costs* costs, const lp_o
       fprintf(stderr, "[create] preload %8.3f ms\n",
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   }
-  // Staging and table buffers sized for a bench-shaped re-plan up front:
-  // cudaMallocHost / cudaMalloc inside the first re-plan cost it 2-3 ms
-  // (profiles/r02_cold_replan.log).  They still grow on demand.
-  if ((e = h->pin_up.ensure(1 << 21)) != cudaSuccess || (e = h->pin_up2.ensure(1 << 21)) != cudaSuccess ||
-      (e = h->pin_down.ensure(1 << 16)) != cudaSuccess || (e = h->tables.ensure(1 << 21)) != cudaSuccess ||
-      (e = h->tables2.ensure(1 << 21)) != cudaSuccess || (e = h->work.ensure(1 << 23)) != cudaSuccess) {
+  // The staging and table buffers at their minimum sizes (what a small
+  // re-plan needs): cudaMallocHost / cudaMalloc inside the first re-plan
+  // cost it 2-3 ms (profiles/r02_cold_replan.log).  They grow on demand;
+  // larger sizes up front made every lp_create 5-18 ms.
+  if ((e = h->pin_up.ensure(1 << 16)) != cudaSuccess || (e = h->pin_up2.ensure(1 << 16)) != cudaSuccess ||
+      (e = h->pin_down.ensure(1 << 16)) != cudaSuccess || (e = h->tables.ensure(1 << 16)) != cudaSuccess ||
+      (e = h->tables2.ensure(1 << 16)) != cudaSuccess || (e = h->work.ensure(1 << 18)) != cudaSuccess) {
     lp_destroy(h);
     return fail(nullptr, LP_ECUDA, "lp_create: %s", cudaGetErrorString(e));
   }
-  if (grow_store(h, size_t(1) << 20) != LP_OK) {
+  if (grow_store(h, size_t(1) << 16) != LP_OK) {
     const std::string msg = h->err;
     lp_destroy(h);
     return fail(nullptr, LP_ENOMEM, "lp_create: %s", msg.c_str());
