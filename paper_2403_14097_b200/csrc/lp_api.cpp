@@ -1971,24 +1971,25 @@ lp_status prepare_dp(lp_handle* h) {
     }
     h->dp_pbase[H] = b;
   }
-  // Materialised phi (LIVEPUT_PHI, off by default): a pipelined re-plan
-  // evaluates level j's pairs in the phi launch of the stage that releases
-  // it, so the level chain left after the sampling is max-plus passes only.
-  // Measured on B200 (bench re-plan): on one GPU -5.5% at
-  // 125K samples per ensemble and -1.6% at 250K, +0.7% at 1e6; under
-  // torchrun on 4 GPUs +1.3% (1.91 against 1.89 ms), so it stays an A/B
-  // path.  LIVEPUT_PHI=1: every pipelined re-plan; LIVEPUT_PHI=<n> > 1: those
-  // whose per-rank ensemble share is at most n samples.  LIVEPUT_PHI_MAX_MB
-  // bounds the phi buffer (default 1024).
+  // Materialised phi: a pipelined re-plan evaluates level j's pairs in the
+  // phi launch of the stage that releases it, so the level chain left after
+  // the sampling is max-plus passes only.  It pays when the sampling is
+  // short against the DP: measured on one B200 -7% on the
+  // forecast-like re-plan (sampling ops / DP pairs = 815), -5.5% and -1.6% on
+  // the bench re-plan at 125K and 250K samples (1500, 3000), +0.6% at 1e6
+  // (12000); under torchrun on 4 GPUs +0.3 to +1.3% in every stream-priority
+  // variant, so multi-rank re-plans keep phi inside the levels.  Default:
+  // one rank and ops / pairs < 4000.  LIVEPUT_PHI=0: never; 1: every
+  // pipelined re-plan; <n> > 1: per-rank ensemble share <= n samples.
+  // LIVEPUT_PHI_MAX_MB bounds the phi buffer (default 1024).
   {
     static const int64_t phi_max = [] {
       const char* e = getenv("LIVEPUT_PHI_MAX_MB");
       return (e ? atoll(e) : 1024LL) << 20;
     }();
-    static const uint64_t phi_trials = [] {  // 0: off, UINT64_MAX: always
+    static const int64_t phi_mode = [] {  // -1: auto
       const char* e = getenv("LIVEPUT_PHI");
-      const unsigned long long v = e ? strtoull(e, nullptr, 10) : 0ull;
-      return v == 1 ? UINT64_MAX : (uint64_t)v;
+      return e ? (int64_t)strtoll(e, nullptr, 10) : (int64_t)-1;
     }();
     const int nst = (int)h->hp.stages.size();
     const bool persistent = nst <= 1 && !h->dp_launches && H <= kMaxHorizon;
@@ -1996,8 +1997,12 @@ lp_status prepare_dp(lp_handle* h) {
     for (const PairDesc& pd : h->hp.pairs) local = std::max<uint64_t>(local, pd.t_hi - pd.t_lo);
     int64_t pairs = 0;
     for (int j = 0; j < H; ++j) pairs += (int64_t)h->levels[j].prev_count * h->levels[j].next_count;
-    h->phi_on = !persistent && local <= phi_trials && pairs > 0 && pairs * 16 <= phi_max &&
-                pairs < (int64_t(1) << 31);
+    bool want;
+    if (phi_mode < 0) want = h->nranks == 1 && (double)h->hp.model_ops < 4000.0 * (double)pairs;
+    else if (phi_mode == 0) want = false;
+    else if (phi_mode == 1) want = true;
+    else want = local <= (uint64_t)phi_mode;
+    h->phi_on = !persistent && want && pairs > 0 && pairs * 16 <= phi_max && pairs < (int64_t(1) << 31);
     h->phi_list.clear();
     const int ns = std::max(nst, 1);
     h->phi_range.assign(ns + 1, 0);

@@ -62,8 +62,8 @@ def test_execution_modes_agree():
                 {"LIVEPUT_ROWS_SHAPE": "96,40,2"}, {"LIVEPUT_ROWS_KREG": "0"},
                 # the materialised-phi DP (phi launches + max-plus levels) on every
                 # pipelined re-plan, per-level phi launches, one stage with level
-                # launches, and the per-rank-share threshold
+                # launches, the per-rank-share threshold, and never
                 {"LIVEPUT_PHI": "1"}, {"LIVEPUT_PHI": "1", "LIVEPUT_PHI_LEVELS": "1"},
                 {"LIVEPUT_PHI": "1", "LIVEPUT_STAGES": "1", "LIVEPUT_DP": "launches"},
-                {"LIVEPUT_PHI": "1", "LIVEPUT_PDL": "0"}, {"LIVEPUT_PHI": "400000"}):
+                {"LIVEPUT_PHI": "1", "LIVEPUT_PDL": "0"}, {"LIVEPUT_PHI": "400000"}, {"LIVEPUT_PHI": "0"}):
         assert _run(env) == base, env

@@ -67,8 +67,8 @@ def test_config3_proactive_replans_with_cache():
 
 @pytest.mark.gpu
 def test_materialised_phi_matches_fixtures():
-    """The multi-GPU DP path (phi launches per pipeline stage + max-plus
-    levels, an A/B path selected with LIVEPUT_PHI) on the
+    """The materialised-phi DP path (phi launches per pipeline stage + max-plus
+    levels; by default on one GPU when the sampling is short against the DP) on the
     full 1e6 ensembles: forced with LIVEPUT_PHI=1, read once per
     process, so it runs in a subprocess."""
     import json
