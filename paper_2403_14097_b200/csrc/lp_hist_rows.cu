@@ -412,8 +412,13 @@ __device__ __forceinline__ void walk_run(int mode, const EntryDesc* ents, int e0
 
 // KREG > 0: register-resident Fisher-Yates map for k <= KREG; 0: shared-memory
 // map (any k).  WMAX: largest ceil(P/32) among the work item's depths.
+// Occupancy is two 256-thread blocks per SM either way (shared memory); the
+// <0, 4> instance (k > 16, n <= 256: the bench's hot kernel) is compiled to
+// the three-block register budget, where it fits 72 registers without a
+// spill (95 at two blocks) and runs 0.45% faster (profiles/r02_rows_regs_ab.log);
+// the other instances would spill there.
 template <int KREG, int WMAX, bool SMEM_EVT>
-__global__ void __launch_bounds__(256, 2) hist_rows_kernel(const WorkItem* __restrict__ work,
+__global__ void __launch_bounds__(256, (KREG == 0 && WMAX <= 4) ? 3 : 2) hist_rows_kernel(const WorkItem* __restrict__ work,
                                                            const PairDesc* __restrict__ pairs,
                                                            const EntryDesc* __restrict__ entries,
                                                            const DrawConst* __restrict__ draws,
